@@ -1,0 +1,169 @@
+/*
+ * dmf.h -- C ABI of libdmf.so, a B200-native (sm_100a) dynamic max-flow engine
+ * implementing the data-parallel hot path of arXiv 2511.05895, "Efficient Dynamic
+ * MaxFlow Computation on GPUs" (citations "P:n" are lines of the paper's LaTeX
+ * source, PAPER.md; "S:n" lines of SPEC.md; "§8(c) Rk" readings in DESIGN.md).
+ *
+ * Problem: directed graph G=(V,E), capacities c(u,v) >= 0, source s,
+ * sink t; maximise |f| subject to 0 <= f <= c and conservation on V\{s,t}.
+ * The engine keeps a residual graph (c_f(u,v) = c(u,v) - f(u,v) + f(v,u))
+ * and a pseudoflow excess e(v) on the device, solves it from scratch with the
+ * GPU-Static-Maxflow loop (Alg.1) and repairs it after a batch of
+ * capacity changes with Dynamic Push-Relabel (Alg.4-5) or Dynamic
+ * Push-Pull (Alg.6-8).
+ *
+ * Conventions for every entry point
+ *  - Return value: DMF_OK (0) or a negative dmf_status; dmf_last_error() gives a
+ *    thread-local one-line message for the most recent failure.
+ *  - Vertex ids are int32 in [0, n).  Capacities are int32 in [0, DMF_CAP_MAX].
+ *    Excess and flow values are int64 (grid configs exceed 2^31).
+ *  - Pointers marked "host or device" may be plain host memory, pinned host memory
+ *    or device memory of the handle's GPU (detected with cudaPointerGetAttributes).
+ *    All caller buffers are caller-owned; the library copies what it needs.
+ *  - All device work is ordered on the handle's stream (dmf_options.stream).  Every
+ *    call returns only when its results are ready (it synchronises that stream).
+ *  - A handle is not thread-safe; distinct handles are independent.
+ */
+#ifndef DMF_H
+#define DMF_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct dmf_graph dmf_graph;   /* opaque: owns every device array of one instance */
+
+typedef enum {
+    DMF_OK = 0,
+    DMF_EINVAL = -1,     /* bad argument: id out of range, self-loop, s == t, cap < 0 or > DMF_CAP_MAX */
+    DMF_ENOSLOT = -2,    /* batch entry (u,v) names no slot (neither an input edge nor the reverse of one) */
+    DMF_EDUP = -3,       /* batch names the same (u,v) twice */
+    DMF_ESTATE = -4,     /* DMF_DYN_PP without a previous converged solve */
+    DMF_ENOMEM = -5,     /* device allocation failed */
+    DMF_ECUDA = -6,      /* CUDA runtime error (message in dmf_last_error) */
+    DMF_EOVERFLOW = -7,  /* merged capacity of a pair exceeds DMF_CAP_MAX, or too many slots (>= 2^31) */
+    DMF_ENOCONV = -8     /* iteration cap reached (never expected; Thm P:318-330 bounds the work) */
+} dmf_status;
+
+typedef enum {
+    DMF_DYN_PR = 0,      /* Dynamic Push-Relabel, Alg.4 */
+    DMF_DYN_PP = 1       /* Dynamic Push-Pull, Alg.8 */
+} dmf_algo;
+
+/* Upper bound of any capacity, so that c(u,v) + c(v,u) < 2^31 always holds and a
+ * residual fits int32. */
+#define DMF_CAP_MAX 1073741823
+
+typedef struct {
+    int32_t kernel_cycles;  /* KERNELCYCLES of Alg.2/Alg.6; 0 => max(1, floor(m/n)) (R17) */
+    int32_t algo;           /* default algorithm for dmf_apply_batch when its algo argument is < 0 */
+    int32_t max_iters;      /* cap on outer loop iterations per call; 0 => 4*n + 64 */
+    int32_t grid_blocks;    /* 0 => occupancy-derived cooperative grid (multiple of the SM count) */
+    void *stream;           /* cudaStream_t for all work; NULL => a stream owned by the handle */
+    /* Optional device allocator (e.g. the torch caching allocator); NULL => cudaMalloc.
+     * alloc returns a device pointer of >= bytes (256-byte aligned) or NULL. */
+    void *(*alloc)(size_t bytes, void *ctx);
+    void (*free)(void *ptr, size_t bytes, void *ctx);
+    void *alloc_ctx;
+} dmf_options;
+
+typedef struct {
+    int64_t n, m, S;           /* vertices; merged input edges; slots (m + materialised reverses) */
+    int32_t kernel_cycles;     /* effective KERNELCYCLES */
+    int32_t grid_blocks, block_threads;
+    /* counters of the LAST solve / apply call */
+    int64_t iterations;        /* outer loop iterations (each = BFS + discharge + RIE), all stages */
+    int64_t bfs_levels;        /* BFS frontier levels over all global relabels */
+    int64_t bfs_vertices;      /* frontier vertices expanded */
+    int64_t bfs_slots;         /* slots scanned by BFS expansion */
+    int64_t discharge_vertices;/* worklist entries discharged */
+    int64_t discharge_slots;   /* slots scanned by discharge (argmin + push passes) */
+    int64_t pushes;            /* push / pull operations (Alg.2 l.16-19, Alg.6 l.16-19) */
+    int64_t relabels;          /* lift operations (Alg.2 l.21, Alg.6 l.21) */
+    int64_t rie_slots;         /* slots scanned by RemoveInvalidEdges */
+    int64_t rie_saturations;   /* edges saturated by RemoveInvalidEdges (Alg.3/Alg.7) */
+    int64_t batch_entries;     /* k of the last batch */
+    int64_t stage2_vertices;   /* |P| of the last push-pull stage 2 (Alg.8 l.29-34) */
+    int64_t stage2_iterations;
+    float   device_ms;         /* device time of the last call's kernel(s), CUDA events */
+    float   reserved;
+} dmf_stats;
+
+/* Fill *opt with defaults (all zero / NULL; algo = DMF_DYN_PP). */
+void dmf_default_options(dmf_options *opt);
+
+/* Build the Bi-CSR residual graph ("Bi-Directional CSR ... zero-capacity
+ * entries to address any missing reverse edges ... an additional array ... stores
+ * the offset of the reverse edges").
+ *  n        number of vertices (>= 2)
+ *  row_ptr  int64[n+1], host or device: CSR offsets of the input edges
+ *  col      int32[row_ptr[n]], host or device: heads
+ *  cap      int32[row_ptr[n]], host or device: capacities in [0, DMF_CAP_MAX]
+ *  s, t     source and sink, s != t
+ * Duplicate (u,v) input entries are merged by summing; zero-capacity input
+ * edges are kept (they are the insertion pool).  Self-loops, ids out of
+ * range, s == t or a negative capacity -> DMF_EINVAL; a merged pair above
+ * DMF_CAP_MAX or >= 2^31 slots -> DMF_EOVERFLOW.  The new state is the zero flow
+ * (not yet solved).  On success *out owns all device memory (dmf_destroy frees it). */
+int dmf_create(int32_t n, const int64_t *row_ptr, const int32_t *col, const int32_t *cap,
+               int32_t s, int32_t t, const dmf_options *opt, dmf_graph **out);
+
+/* GPU-Static-Maxflow (Alg.1) on the current capacities, from the zero
+ * flow: c_f = c, e = 0, saturate s's out-edges, then loop {global relabel by
+ * backward BFS from the sink set, PushRelabel x KERNELCYCLES on the active
+ * worklist, RemoveInvalidEdges} until a fresh BFS reaches no active vertex
+ * (readings R1, R2, R9 of DESIGN.md: the sink set is {t} u deficient vertices). */
+int dmf_static_solve(dmf_graph *g);
+
+/* Apply a batch of k capacity updates (SET semantics, all entries simultaneous,
+ * P:342 "each batch is a set of edges whose new capacities may be either higher or
+ * lower") and repair the state to convergence with `algo` (DMF_DYN_PR = Alg.4,
+ * DMF_DYN_PP = Alg.8; < 0 => options.algo).
+ *  u, v, new_cap  int32[k], host or device
+ * The whole batch is validated on the device BEFORE any mutation: an entry whose
+ * (u,v) is not a slot -> DMF_ENOSLOT, a repeated (u,v) -> DMF_EDUP, ids out of range
+ * -> DMF_EINVAL, new_cap outside [0, DMF_CAP_MAX] -> DMF_EOVERFLOW; on any error the
+ * residual/excess/capacity state is unchanged.  DMF_DYN_PP needs a previous
+ * converged solve on this handle (else DMF_ESTATE).  k = 0 is allowed. */
+int dmf_apply_batch(dmf_graph *g, int64_t k, const int32_t *u, const int32_t *v,
+                    const int32_t *new_cap, int32_t algo);
+
+/* Maximum-flow value of the converged state: F = e(t) + sum_{v not in {s,t}}
+ * min(e(v), 0) (Alg.4 final loop P:381-386 / Alg.8; reading R8). */
+int dmf_flow_value(const dmf_graph *g, int64_t *out);
+
+/* Minimal min-cut source side S_min (unique): mask[v] = 1 iff v is reachable in the
+ * residual graph from {s} u {v not in {s,t} : e(v) > 0} (reading R19; equals
+ * the residual reach of s for any true maximum flow).  mask: uint8[n], host or device. */
+int dmf_min_cut_source_side(dmf_graph *g, uint8_t *mask);
+
+/* Maximal min-cut source side S_max: mask[v] = 1 iff v cannot reach {t} u {deficient}
+ * in the residual graph -- the paper's certificate S = {h = |V|} (Thm 3, P:245-248;
+ * Note 1).  mask: uint8[n], host or device. */
+int dmf_max_cut_source_side(dmf_graph *g, uint8_t *mask);
+
+/* Counters of the last call (see dmf_stats). */
+int dmf_get_stats(const dmf_graph *g, dmf_stats *out);
+
+/* Sizes: *n vertices, *S slots, *m merged input edges (any may be NULL). */
+int dmf_sizes(const dmf_graph *g, int32_t *n, int64_t *S, int64_t *m);
+
+/* Copy the device state to caller buffers (host or device; any may be NULL):
+ * row_ptr int64[n+1], dst/rev/cap/res int32[S] (slot form: rows sorted by head,
+ * rev[i] = slot of the reverse pair), excess int64[n].  For checkers. */
+int dmf_export_state(const dmf_graph *g, int64_t *row_ptr, int32_t *dst, int32_t *rev,
+                     int32_t *cap, int32_t *res, int64_t *excess);
+
+/* Free every device array of the handle (NULL is a no-op). */
+void dmf_destroy(dmf_graph *g);
+
+/* Thread-local message of the last failing call on this thread ("" if none). */
+const char *dmf_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DMF_H */

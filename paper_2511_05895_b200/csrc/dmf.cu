@@ -1,0 +1,536 @@
+// dmf.cu -- libdmf.so: C ABI (include/dmf.h) + the one-time Bi-CSR builder.
+//
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -shared
+//        -Xcompiler -fPIC -I include -o paper_2511_05895_b200/libdmf.so dmf.cu
+//
+// Every step of the hot path runs in kernels of this file / solve.cuh.  CUB is used
+// only by dmf_create (the one-time Bi-CSR build: sort + run-length merge), never
+// on the per-batch path.
+#include "dmf.h"
+#include "dmf_device.cuh"
+#include "solve.cuh"
+
+#include <cub/cub.cuh>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+using namespace dmf;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+#define CK(call)                                                                             \
+  do {                                                                                       \
+    cudaError_t err__ = (call);                                                              \
+    if (err__ != cudaSuccess) return fail(DMF_ECUDA, "%s: %s (%s:%d)", #call,                \
+                                          cudaGetErrorString(err__), __FILE__, __LINE__);    \
+  } while (0)
+
+bool is_device_ptr(const void *p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return false; }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+}  // namespace
+
+struct dmf_graph {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  dmf_options opt{};
+  int32_t n = 0, s = 0, t = 0, kc = 1;
+  int64_t S = 0, m = 0;
+  int32_t *row = nullptr, *dst = nullptr, *rev = nullptr, *cap = nullptr, *res = nullptr, *rres = nullptr;
+  int32_t *hp = nullptr, *hm = nullptr, *q0 = nullptr, *q1 = nullptr, *wl = nullptr, *rl = nullptr;
+  int32_t *plist = nullptr, *stamp = nullptr;
+  long long *e = nullptr;
+  uint8_t *part = nullptr, *mask = nullptr;
+  int32_t *bbuf = nullptr;   // batch staging: u, v, c, slot  (4 * bcap)
+  int64_t bcap = 0;
+  Ctl *ctl = nullptr;
+  Ctl *hctl = nullptr;       // pinned mirror
+  int grid_blocks = 0;
+  int32_t batch_id = 0;
+  bool solved = false;
+  int64_t flow = 0;
+  dmf_stats stats{};
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::vector<std::pair<void *, size_t>> allocs;
+
+  void *alloc(size_t bytes) {
+    bytes = (bytes + 255) & ~size_t(255);
+    if (bytes == 0) bytes = 256;
+    void *p = nullptr;
+    if (opt.alloc) p = opt.alloc(bytes, opt.alloc_ctx);
+    else if (cudaMalloc(&p, bytes) != cudaSuccess) { cudaGetLastError(); p = nullptr; }
+    if (p) allocs.emplace_back(p, bytes);
+    return p;
+  }
+  void release(void *p) {
+    for (size_t i = 0; i < allocs.size(); i++)
+      if (allocs[i].first == p) {
+        if (opt.free) opt.free(p, allocs[i].second, opt.alloc_ctx); else cudaFree(p);
+        allocs.erase(allocs.begin() + (long)i);
+        return;
+      }
+  }
+  void release_all() {
+    for (auto &a : allocs) { if (opt.free) opt.free(a.first, a.second, opt.alloc_ctx); else cudaFree(a.first); }
+    allocs.clear();
+  }
+};
+
+// ============================================================================ build kernels
+namespace {
+
+__global__ void k_expand_edges(int32_t n, int64_t m, const int64_t *rp, const int32_t *col, const int32_t *cap,
+                               unsigned long long *key, int32_t *val, int32_t *err) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x) {
+    int32_t lo = 0, hi = n;             // u = last row with rp[u] <= j
+    while (lo < hi) {
+      const int32_t mid = (lo + hi + 1) >> 1;
+      if (rp[mid] <= j) lo = mid; else hi = mid - 1;
+    }
+    const int32_t u = lo, v = col[j], c = cap[j];
+    if (v < 0 || v >= n || v == u) { atomicCAS(err, 0, DMF_EINVAL); continue; }
+    if (c < 0) { atomicCAS(err, 0, DMF_EINVAL); continue; }
+    if (c > DMF_CAP_MAX) { atomicCAS(err, 0, DMF_EOVERFLOW); continue; }
+    key[2 * j] = (unsigned long long)u * (unsigned long long)n + (unsigned long long)v;
+    val[2 * j] = c;
+    key[2 * j + 1] = (unsigned long long)v * (unsigned long long)n + (unsigned long long)u;
+    val[2 * j + 1] = -1;                // materialised reverse (zero capacity)
+  }
+}
+
+__global__ void k_run_heads(int64_t N, const unsigned long long *key, int32_t *head) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < N; p += (int64_t)gridDim.x * blockDim.x)
+    head[p] = (p == 0 || key[p] != key[p - 1]) ? 1 : 0;
+}
+
+// scan[p] = inclusive count of run heads -> slot = scan[p] - 1
+__global__ void k_merge_runs(int64_t N, const unsigned long long *key, const int32_t *val, const int32_t *scan,
+                             unsigned long long *ukey, long long *capsum, int32_t *isinput) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < N; p += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t slot = scan[p] - 1;
+    if (p == 0 || key[p] != key[p - 1]) ukey[slot] = key[p];
+    if (val[p] >= 0) {
+      atomicAdd(reinterpret_cast<unsigned long long *>(capsum + slot), (unsigned long long)val[p]);
+      isinput[slot] = 1;
+    }
+  }
+}
+
+__device__ int64_t lower_bound_u64(const unsigned long long *a, int64_t N, unsigned long long x) {
+  int64_t lo = 0, hi = N;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (a[mid] < x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void k_rows(int32_t n, int64_t S, const unsigned long long *ukey, int32_t *row) {
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u <= n; u += (int64_t)gridDim.x * blockDim.x)
+    row[u] = (int32_t)(u == n ? S : lower_bound_u64(ukey, S, (unsigned long long)u * (unsigned long long)n));
+}
+
+__global__ void k_slots(int32_t n, int64_t S, const unsigned long long *ukey, const long long *capsum,
+                        int32_t *dst, int32_t *rev, int32_t *cap, int32_t *err) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < S; i += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long k = ukey[i];
+    const unsigned long long u = k / (unsigned long long)n, v = k % (unsigned long long)n;
+    dst[i] = (int32_t)v;
+    rev[i] = (int32_t)lower_bound_u64(ukey, S, v * (unsigned long long)n + u);
+    const long long c = capsum[i];
+    if (c > DMF_CAP_MAX) atomicCAS(err, 0, DMF_EOVERFLOW);
+    cap[i] = (int32_t)(c > DMF_CAP_MAX ? DMF_CAP_MAX : c);
+  }
+}
+
+__global__ void k_init_state(int64_t S, int32_t n, const int32_t *rev, const int32_t *cap, int32_t *res,
+                             int32_t *rres, int32_t *stamp, long long *e, uint8_t *part, int32_t *hp, int32_t *hm) {
+  const int64_t st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < S; i += st) {
+    res[i] = cap[i];
+    rres[i] = cap[rev[i]];
+    stamp[i] = 0;
+  }
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += st) {
+    e[v] = 0; part[v] = PART_NONE; hp[v] = n; hm[v] = n;
+  }
+}
+
+__global__ void k_sum_i32(int64_t N, const int32_t *a, unsigned long long *out) {
+  unsigned long long s = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) s += a[i];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
+}
+
+int bits_for(unsigned long long x) {
+  int b = 1;
+  while (b < 64 && (x >> b)) b++;
+  return b;
+}
+
+}  // namespace
+
+// ============================================================================ helpers
+
+static Dev make_dev(dmf_graph *g) {
+  Dev d{};
+  d.n = g->n; d.s = g->s; d.t = g->t; d.kc = g->kc;
+  d.max_iters = g->opt.max_iters > 0 ? g->opt.max_iters : (int32_t)(4LL * g->n + 64 > 0x3fffffff ? 0x3fffffff : 4LL * g->n + 64);
+  d.batch_id = g->batch_id;
+  d.S = g->S; d.k = 0;
+  d.row = g->row; d.dst = g->dst; d.rev = g->rev; d.cap = g->cap; d.res = g->res; d.rres = g->rres;
+  d.e = g->e; d.hp = g->hp; d.hm = g->hm; d.part = g->part;
+  d.q0 = g->q0; d.q1 = g->q1;
+  d.wl0 = g->wl; d.wl1 = g->wl + g->n; d.wl2 = g->wl + 2 * (size_t)g->n;
+  d.rl = g->rl; d.plist = g->plist; d.stamp = g->stamp;
+  d.mask = g->mask; d.ctl = g->ctl;
+  return d;
+}
+
+static int run_solve(dmf_graph *g, int32_t mode, const Dev &dv) {
+  Dev d = dv;
+  CK(cudaMemsetAsync(g->ctl, 0, sizeof(Ctl), g->stream));
+  CK(cudaEventRecord(g->ev0, g->stream));
+  int32_t md = mode;
+  void *args[] = {&d, &md};
+  CK(cudaLaunchCooperativeKernel((const void *)k_solve<NT>, dim3(g->grid_blocks), dim3(NT), args, 0, g->stream));
+  CK(cudaEventRecord(g->ev1, g->stream));
+  CK(cudaMemcpyAsync(g->hctl, g->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, g->stream));
+  CK(cudaStreamSynchronize(g->stream));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, g->ev0, g->ev1);
+  const Ctl &c = *g->hctl;
+  dmf_stats &st = g->stats;
+  st.iterations = (int64_t)c.stat[ST_ITERS];
+  st.bfs_levels = (int64_t)c.stat[ST_LEVELS];
+  st.bfs_vertices = (int64_t)c.stat[ST_BFS_V];
+  st.bfs_slots = (int64_t)c.stat[ST_BFS_SLOTS];
+  st.discharge_vertices = (int64_t)c.stat[ST_DIS_V];
+  st.discharge_slots = (int64_t)c.stat[ST_DIS_SLOTS];
+  st.pushes = (int64_t)c.stat[ST_PUSHES];
+  st.relabels = (int64_t)c.stat[ST_RELABELS];
+  st.rie_slots = (int64_t)c.stat[ST_RIE_SLOTS];
+  st.rie_saturations = (int64_t)c.stat[ST_RIE_SAT];
+  st.stage2_vertices = (int64_t)c.stat[ST_S2_V];
+  st.stage2_iterations = (int64_t)c.stat[ST_S2_ITERS];
+  st.batch_entries = dv.k;
+  st.device_ms = ms;
+  if (c.status != 0) {
+    const char *what = c.status == DMF_ENOSLOT ? "no slot for (u,v)"
+                     : c.status == DMF_EDUP ? "duplicate (u,v) in batch"
+                     : c.status == DMF_EINVAL ? "vertex id out of range"
+                     : c.status == DMF_EOVERFLOW ? "capacity outside [0, DMF_CAP_MAX]"
+                     : c.status == DMF_ENOCONV ? "iteration cap reached" : "error";
+    return fail(c.status, "%s (batch entry %d)", what, c.err_entry);
+  }
+  if (mode == MODE_STATIC || mode == MODE_PR || mode == MODE_PP) {
+    g->flow = c.flow;
+    g->solved = true;
+  }
+  return DMF_OK;
+}
+
+// ============================================================================ C ABI
+
+extern "C" {
+
+void dmf_default_options(dmf_options *opt) {
+  if (!opt) return;
+  memset(opt, 0, sizeof(*opt));
+  opt->algo = DMF_DYN_PP;
+}
+
+const char *dmf_last_error(void) { return g_last_error.c_str(); }
+
+int dmf_create(int32_t n, const int64_t *row_ptr, const int32_t *col, const int32_t *cap, int32_t s, int32_t t,
+               const dmf_options *opt, dmf_graph **out) {
+  g_last_error.clear();
+  if (!out) return fail(DMF_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (n < 2 || !row_ptr) return fail(DMF_EINVAL, "n must be >= 2 and row_ptr non-NULL");
+  if (s < 0 || s >= n || t < 0 || t >= n || s == t) return fail(DMF_EINVAL, "bad source/sink (%d, %d)", s, t);
+  dmf_graph *g = new dmf_graph();
+  if (opt) g->opt = *opt; else dmf_default_options(&g->opt);
+  g->n = n; g->s = s; g->t = t;
+  auto bail = [&](int code) { g->release_all(); if (g->own_stream && g->stream) cudaStreamDestroy(g->stream);
+                              if (g->hctl) cudaFreeHost(g->hctl); delete g; return code; };
+#define CKB(call) do { cudaError_t e__ = (call); if (e__ != cudaSuccess) { \
+      fail(DMF_ECUDA, "%s: %s", #call, cudaGetErrorString(e__)); return bail(DMF_ECUDA); } } while (0)
+  CKB(cudaGetDevice(&g->device));
+  if (g->opt.stream) g->stream = (cudaStream_t)g->opt.stream;
+  else { CKB(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking)); g->own_stream = true; }
+  cudaStream_t st = g->stream;
+  // ---- input to the device
+  int64_t m = 0;
+  const bool rp_dev = is_device_ptr(row_ptr);
+  if (rp_dev) CKB(cudaMemcpy(&m, row_ptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost));
+  else {
+    m = row_ptr[n];
+    if (row_ptr[0] != 0) { fail(DMF_EINVAL, "row_ptr[0] != 0"); return bail(DMF_EINVAL); }
+    for (int32_t u = 0; u < n; u++)
+      if (row_ptr[u + 1] < row_ptr[u]) { fail(DMF_EINVAL, "row_ptr decreasing at %d", u); return bail(DMF_EINVAL); }
+  }
+  if (m < 0) { fail(DMF_EINVAL, "negative edge count"); return bail(DMF_EINVAL); }
+  if (2 * m >= (int64_t)0x7fffffff) { fail(DMF_EOVERFLOW, "too many edges (%lld)", (long long)m); return bail(DMF_EOVERFLOW); }
+  const int64_t N2 = 2 * m;
+  int64_t *d_rp = (int64_t *)g->alloc((n + 1) * sizeof(int64_t));
+  int32_t *d_col = (int32_t *)g->alloc((m ? m : 1) * sizeof(int32_t));
+  int32_t *d_cap = (int32_t *)g->alloc((m ? m : 1) * sizeof(int32_t));
+  unsigned long long *k0 = (unsigned long long *)g->alloc((N2 ? N2 : 1) * 8);
+  unsigned long long *k1 = (unsigned long long *)g->alloc((N2 ? N2 : 1) * 8);
+  int32_t *v0 = (int32_t *)g->alloc((N2 ? N2 : 1) * 4);
+  int32_t *v1 = (int32_t *)g->alloc((N2 ? N2 : 1) * 4);
+  int32_t *scan = (int32_t *)g->alloc((N2 ? N2 : 1) * 4);
+  int32_t *err = (int32_t *)g->alloc(64);
+  if (!d_rp || !d_col || !d_cap || !k0 || !k1 || !v0 || !v1 || !scan || !err) { fail(DMF_ENOMEM, "device allocation failed (input staging)"); return bail(DMF_ENOMEM); }
+  CKB(cudaMemcpyAsync(d_rp, row_ptr, (n + 1) * sizeof(int64_t), cudaMemcpyDefault, st));
+  if (m) {
+    CKB(cudaMemcpyAsync(d_col, col, m * sizeof(int32_t), cudaMemcpyDefault, st));
+    CKB(cudaMemcpyAsync(d_cap, cap, m * sizeof(int32_t), cudaMemcpyDefault, st));
+  }
+  CKB(cudaMemsetAsync(err, 0, 64, st));
+  const int TB = 256;
+  auto blocks = [](int64_t N) { int64_t b = (N + 255) / 256; return (int)(b < 1 ? 1 : (b > 148 * 64 ? 148 * 64 : b)); };
+  int64_t S = 0;
+  unsigned long long *ukey = nullptr;
+  long long *capsum = nullptr;
+  int32_t *isinput = nullptr;
+  if (m) {
+    k_expand_edges<<<blocks(m), TB, 0, st>>>(n, m, d_rp, d_col, d_cap, k0, v0, err);
+    CKB(cudaGetLastError());
+    int32_t herr = 0;
+    CKB(cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, st));
+    CKB(cudaStreamSynchronize(st));
+    if (herr) { fail(herr, herr == DMF_EOVERFLOW ? "input capacity above DMF_CAP_MAX" : "invalid input edge (self-loop, id out of range or negative capacity)"); return bail(herr); }
+    const int endbit = bits_for((unsigned long long)n * (unsigned long long)n);
+    size_t tb = 0;
+    CKB(cub::DeviceRadixSort::SortPairs(nullptr, tb, k0, k1, v0, v1, (int)N2, 0, endbit, st));
+    size_t tb2 = 0;
+    CKB(cub::DeviceScan::InclusiveSum(nullptr, tb2, scan, scan, (int)N2, st));
+    void *tmp = g->alloc(tb > tb2 ? tb : tb2);
+    if (!tmp) { fail(DMF_ENOMEM, "device allocation failed (sort)"); return bail(DMF_ENOMEM); }
+    CKB(cub::DeviceRadixSort::SortPairs(tmp, tb, k0, k1, v0, v1, (int)N2, 0, endbit, st));
+    k_run_heads<<<blocks(N2), TB, 0, st>>>(N2, k1, scan);
+    CKB(cub::DeviceScan::InclusiveSum(tmp, tb2, scan, scan, (int)N2, st));
+    int32_t hS = 0;
+    CKB(cudaMemcpyAsync(&hS, scan + N2 - 1, 4, cudaMemcpyDeviceToHost, st));
+    CKB(cudaStreamSynchronize(st));
+    S = hS;
+    ukey = k0;                       // reuse
+    capsum = (long long *)g->alloc(S * 8);
+    isinput = v0;                    // reuse (N2 >= S)
+    if (!capsum) { fail(DMF_ENOMEM, "device allocation failed (merge)"); return bail(DMF_ENOMEM); }
+    CKB(cudaMemsetAsync(capsum, 0, S * 8, st));
+    CKB(cudaMemsetAsync(isinput, 0, S * 4, st));
+    k_merge_runs<<<blocks(N2), TB, 0, st>>>(N2, k1, v1, scan, ukey, capsum, isinput);
+    CKB(cudaGetLastError());
+    g->release(tmp);
+  }
+  g->S = S;
+  // ---- persistent arrays
+  const size_t nn = (size_t)n;
+  g->row = (int32_t *)g->alloc((nn + 1) * 4);
+  g->dst = (int32_t *)g->alloc(S * 4);
+  g->rev = (int32_t *)g->alloc(S * 4);
+  g->cap = (int32_t *)g->alloc(S * 4);
+  g->res = (int32_t *)g->alloc(S * 4);
+  g->rres = (int32_t *)g->alloc(S * 4);
+  g->stamp = (int32_t *)g->alloc(S * 4);
+  g->e = (long long *)g->alloc(nn * 8);
+  g->hp = (int32_t *)g->alloc(nn * 4);
+  g->hm = (int32_t *)g->alloc(nn * 4);
+  g->part = (uint8_t *)g->alloc(nn);
+  g->mask = (uint8_t *)g->alloc(nn);
+  g->q0 = (int32_t *)g->alloc(3 * nn * 4);
+  g->q1 = (int32_t *)g->alloc(3 * nn * 4);
+  g->wl = (int32_t *)g->alloc(3 * nn * 4);
+  g->rl = (int32_t *)g->alloc(3 * nn * 4);
+  g->plist = (int32_t *)g->alloc(nn * 4);
+  g->ctl = (Ctl *)g->alloc(sizeof(Ctl));
+  if (!g->row || !g->dst || !g->rev || !g->cap || !g->res || !g->rres || !g->stamp || !g->e || !g->hp || !g->hm ||
+      !g->part || !g->mask || !g->q0 || !g->q1 || !g->wl || !g->rl || !g->plist || !g->ctl) {
+    fail(DMF_ENOMEM, "device allocation failed (state, S=%lld)", (long long)S);
+    return bail(DMF_ENOMEM);
+  }
+  CKB(cudaMallocHost((void **)&g->hctl, sizeof(Ctl)));
+  if (S) {
+    CKB(cudaMemsetAsync(err, 0, 64, st));
+    k_rows<<<blocks(nn + 1), TB, 0, st>>>(n, S, ukey, g->row);
+    k_slots<<<blocks(S), TB, 0, st>>>(n, S, ukey, capsum, g->dst, g->rev, g->cap, err);
+    unsigned long long *msum = (unsigned long long *)(err + 8);
+    k_sum_i32<<<blocks(S), TB, 0, st>>>(S, isinput, msum);
+    CKB(cudaGetLastError());
+    int32_t hbuf[16];
+    CKB(cudaMemcpyAsync(hbuf, err, 64, cudaMemcpyDeviceToHost, st));
+    CKB(cudaStreamSynchronize(st));
+    if (hbuf[0]) { fail(DMF_EOVERFLOW, "merged capacity of a pair exceeds DMF_CAP_MAX"); return bail(DMF_EOVERFLOW); }
+    unsigned long long hm_ = 0;
+    memcpy(&hm_, hbuf + 8, 8);
+    g->m = (int64_t)hm_;
+  } else {
+    CKB(cudaMemsetAsync(g->row, 0, (nn + 1) * 4, st));
+  }
+  k_init_state<<<blocks(S > (int64_t)nn ? S : (int64_t)nn), TB, 0, st>>>(S, n, g->rev, g->cap, g->res, g->rres, g->stamp,
+                                                                      g->e, g->part, g->hp, g->hm);
+  CKB(cudaGetLastError());
+  CKB(cudaStreamSynchronize(st));
+  // free staging
+  for (void *p : {(void *)d_rp, (void *)d_col, (void *)d_cap, (void *)k0, (void *)k1, (void *)v0, (void *)v1,
+                  (void *)scan, (void *)capsum})
+    if (p) g->release(p);
+  // KERNELCYCLES = max(1, floor(m/n)) (R17)
+  g->kc = g->opt.kernel_cycles > 0 ? g->opt.kernel_cycles : (int32_t)(g->m / n > 0 ? g->m / n : 1);
+  // cooperative grid
+  int per_sm = 0, sms = 0;
+  CKB(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve<NT>, NT, 0));
+  CKB(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device));
+  if (per_sm < 1) { fail(DMF_ECUDA, "solve kernel cannot be resident (occupancy 0)"); return bail(DMF_ECUDA); }
+  g->grid_blocks = per_sm * sms;
+  if (g->opt.grid_blocks > 0 && g->opt.grid_blocks < g->grid_blocks) g->grid_blocks = g->opt.grid_blocks;
+  CKB(cudaEventCreate(&g->ev0));
+  CKB(cudaEventCreate(&g->ev1));
+  g->stats.n = n; g->stats.m = g->m; g->stats.S = S; g->stats.kernel_cycles = g->kc;
+  g->stats.grid_blocks = g->grid_blocks; g->stats.block_threads = NT;
+  *out = g;
+#undef CKB
+  return DMF_OK;
+}
+
+int dmf_static_solve(dmf_graph *g) {
+  g_last_error.clear();
+  if (!g) return fail(DMF_EINVAL, "NULL handle");
+  Dev d = make_dev(g);
+  return run_solve(g, MODE_STATIC, d);
+}
+
+int dmf_apply_batch(dmf_graph *g, int64_t k, const int32_t *u, const int32_t *v, const int32_t *new_cap, int32_t algo) {
+  g_last_error.clear();
+  if (!g) return fail(DMF_EINVAL, "NULL handle");
+  if (k < 0 || (k > 0 && (!u || !v || !new_cap))) return fail(DMF_EINVAL, "bad batch arrays");
+  if (k >= 0x7fffffff) return fail(DMF_EINVAL, "batch too large");
+  if (algo < 0) algo = g->opt.algo;
+  if (algo != DMF_DYN_PR && algo != DMF_DYN_PP) return fail(DMF_EINVAL, "unknown algo %d", algo);
+  if (algo == DMF_DYN_PP && !g->solved) return fail(DMF_ESTATE, "DMF_DYN_PP needs a previous converged solve");
+  Dev d = make_dev(g);
+  if (k > 0) {
+    const bool dev_in = is_device_ptr(u) && is_device_ptr(v) && is_device_ptr(new_cap);
+    if (k > g->bcap) {
+      if (g->bbuf) g->release(g->bbuf);
+      g->bcap = k + k / 4 + 1024;
+      g->bbuf = (int32_t *)g->alloc(4 * g->bcap * sizeof(int32_t));
+      if (!g->bbuf) { g->bcap = 0; return fail(DMF_ENOMEM, "batch buffer allocation failed"); }
+    }
+    if (dev_in) { d.bu = u; d.bv = v; d.bc = new_cap; }
+    else {
+      CK(cudaMemcpyAsync(g->bbuf, u, k * 4, cudaMemcpyDefault, g->stream));
+      CK(cudaMemcpyAsync(g->bbuf + g->bcap, v, k * 4, cudaMemcpyDefault, g->stream));
+      CK(cudaMemcpyAsync(g->bbuf + 2 * g->bcap, new_cap, k * 4, cudaMemcpyDefault, g->stream));
+      d.bu = g->bbuf; d.bv = g->bbuf + g->bcap; d.bc = g->bbuf + 2 * g->bcap;
+    }
+    d.bslot = g->bbuf + 3 * g->bcap;
+  }
+  d.k = k;
+  d.batch_id = ++g->batch_id;
+  if (g->batch_id >= 0x7ffffff0) {   // stamp wrap-around: clear the stamps
+    CK(cudaMemsetAsync(g->stamp, 0, g->S * 4, g->stream));
+    g->batch_id = 1;
+    d.batch_id = 1;
+  }
+  return run_solve(g, algo == DMF_DYN_PP ? MODE_PP : MODE_PR, d);
+}
+
+int dmf_flow_value(const dmf_graph *g, int64_t *out) {
+  g_last_error.clear();
+  if (!g || !out) return fail(DMF_EINVAL, "NULL argument");
+  if (!g->solved) return fail(DMF_ESTATE, "no converged solve yet");
+  *out = g->flow;
+  return DMF_OK;
+}
+
+static int cut_query(dmf_graph *g, uint8_t *mask, int32_t mode) {
+  g_last_error.clear();
+  if (!g || !mask) return fail(DMF_EINVAL, "NULL argument");
+  if (!g->solved) return fail(DMF_ESTATE, "no converged solve yet");
+  dmf_stats keep = g->stats;
+  Dev d = make_dev(g);
+  int rc = run_solve(g, mode, d);
+  g->stats = keep;
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(mask, g->mask, (size_t)g->n, cudaMemcpyDefault, g->stream));
+  CK(cudaStreamSynchronize(g->stream));
+  return DMF_OK;
+}
+
+int dmf_min_cut_source_side(dmf_graph *g, uint8_t *mask) { return cut_query(g, mask, MODE_MINCUT); }
+int dmf_max_cut_source_side(dmf_graph *g, uint8_t *mask) { return cut_query(g, mask, MODE_MAXCUT); }
+
+int dmf_get_stats(const dmf_graph *g, dmf_stats *out) {
+  if (!g || !out) return fail(DMF_EINVAL, "NULL argument");
+  *out = g->stats;
+  return DMF_OK;
+}
+
+int dmf_sizes(const dmf_graph *g, int32_t *n, int64_t *S, int64_t *m) {
+  if (!g) return fail(DMF_EINVAL, "NULL handle");
+  if (n) *n = g->n;
+  if (S) *S = g->S;
+  if (m) *m = g->m;
+  return DMF_OK;
+}
+
+int dmf_export_state(const dmf_graph *g, int64_t *row_ptr, int32_t *dst, int32_t *rev, int32_t *cap, int32_t *res,
+                     int64_t *excess) {
+  g_last_error.clear();
+  if (!g) return fail(DMF_EINVAL, "NULL handle");
+  cudaStream_t st = g->stream;
+  if (row_ptr) {
+    std::vector<int32_t> r(g->n + 1);
+    CK(cudaMemcpyAsync(r.data(), g->row, (g->n + 1) * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    std::vector<int64_t> r64(r.begin(), r.end());
+    CK(cudaMemcpyAsync(row_ptr, r64.data(), (g->n + 1) * 8, cudaMemcpyDefault, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  if (dst) CK(cudaMemcpyAsync(dst, g->dst, g->S * 4, cudaMemcpyDefault, st));
+  if (rev) CK(cudaMemcpyAsync(rev, g->rev, g->S * 4, cudaMemcpyDefault, st));
+  if (cap) CK(cudaMemcpyAsync(cap, g->cap, g->S * 4, cudaMemcpyDefault, st));
+  if (res) CK(cudaMemcpyAsync(res, g->res, g->S * 4, cudaMemcpyDefault, st));
+  if (excess) CK(cudaMemcpyAsync(excess, g->e, (size_t)g->n * 8, cudaMemcpyDefault, st));
+  CK(cudaStreamSynchronize(st));
+  return DMF_OK;
+}
+
+void dmf_destroy(dmf_graph *g) {
+  if (!g) return;
+  if (g->stream) cudaStreamSynchronize(g->stream);
+  g->release_all();
+  if (g->hctl) cudaFreeHost(g->hctl);
+  if (g->ev0) cudaEventDestroy(g->ev0);
+  if (g->ev1) cudaEventDestroy(g->ev1);
+  if (g->own_stream && g->stream) cudaStreamDestroy(g->stream);
+  delete g;
+}
+
+}  // extern "C"

@@ -1,0 +1,198 @@
+// dmf_device.cuh -- device-side state layout and cooperative-group primitives of
+// libdmf (B200 / sm_100a).  See DESIGN.md §3 for the HBM layout and §4 for the
+// kernels.  Nothing here is shared with oracle/ (the CPU oracle).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <cooperative_groups.h>
+
+namespace dmf {
+
+namespace cg = cooperative_groups;
+
+// Persistent cooperative kernel geometry: 512 threads, >= 2 CTAs per SM
+// (registers <= 64), grid = resident CTAs (a multiple of the 148 SMs).
+constexpr int NT = 512;
+constexpr int WPB = NT / 32;
+constexpr int MIN_BLOCKS = 2;
+
+// Worklist degree bins: thread / warp / CTA per vertex.
+constexpr int32_t BIN0_MAX = 16;
+constexpr int32_t BIN1_MAX = 2048;
+
+// Entries of queues / worklists carry the track in bit 31 (vertex ids < 2^31).
+constexpr uint32_t TRACK_BIT = 0x80000000u;
+
+// Partition labels of Alg.8.  S'/T' are stored as S/T.
+enum : uint8_t { PART_NONE = 0, PART_S = 1, PART_T = 2, PART_P = 3 };
+
+enum Mode : int32_t {
+  MODE_STATIC = 0,   // Alg.1 from the zero flow
+  MODE_PR = 1,       // batch + Alg.4
+  MODE_PP = 2,       // batch + Alg.8
+  MODE_MINCUT = 3,   // forward reach of {s} u Exc  (S_min)
+  MODE_MAXCUT = 4,   // complement of backward reach of {t} u Def (S_max)
+};
+
+enum Stat : int {
+  ST_ITERS, ST_LEVELS, ST_BFS_V, ST_BFS_SLOTS, ST_DIS_V, ST_DIS_SLOTS, ST_PUSHES,
+  ST_RELABELS, ST_RIE_SLOTS, ST_RIE_SAT, ST_S2_V, ST_S2_ITERS, ST_N
+};
+
+// Control block in device memory (zeroed by the host before every launch).
+struct Ctl {
+  int32_t qc[9];        // BFS frontier counts [level % 3][degree bin]
+  int32_t wlc[3];       // active worklist counts per degree bin
+  int32_t rlc[3];       // relabelled-vertex list counts per degree bin
+  int32_t pcnt;         // |P| (push-pull stage 2 region)
+  int32_t status;       // dmf_status of the call (0 = OK)
+  int32_t err_entry;    // first offending batch entry
+  int32_t iters;
+  int32_t pad;
+  long long flow;       // F
+  unsigned long long stat[ST_N];
+};
+
+// Everything a kernel needs, passed by value.  Slot arrays are SoA int32[S]:
+//   row[u]..row[u+1]  slots of u, sorted by dst (binary-searchable)
+//   dst[i]            head of slot i
+//   rev[i]            slot of the reverse pair (involution)
+//   cap[i]            c(u,v)
+//   res[i]            c_f(u,v)
+//   rres[i]           mirror res[rev[i]] = c_f(v,u), kept in lock-step so that the
+//                     backward BFS and the pull track read it coalesced
+struct Dev {
+  int32_t n, s, t, kc, max_iters;
+  int32_t batch_id;
+  int64_t S, k;
+  const int32_t *__restrict__ row;
+  const int32_t *__restrict__ dst;
+  const int32_t *__restrict__ rev;
+  int32_t *cap, *res, *rres;
+  long long *e;              // excess e(v), int64
+  int32_t *hp, *hm;          // h+ (push heights), h- (pull heights), in [0, n]
+  uint8_t *part;             // PART_*
+  int32_t *q0, *q1;          // BFS frontier ping-pong
+  int32_t *wl0, *wl1, *wl2;  // active worklists by degree bin
+  int32_t *rl;               // relabelled vertices (RemoveInvalidEdges scope, R13)
+  int32_t *plist;            // region P of push-pull stage 2
+  int32_t *stamp;            // per-slot batch stamp (duplicate detection)
+  const int32_t *bu, *bv, *bc;  // batch entries
+  int32_t *bslot;            // slot of each batch entry
+  uint8_t *mask;             // cut output
+  Ctl *ctl;
+};
+
+// ---------------------------------------------------------------- loads
+__device__ __forceinline__ int32_t ldv(const int32_t *p) { return __ldcg(p); }
+__device__ __forceinline__ long long ldv(const long long *p) { return __ldcg(p); }
+__device__ __forceinline__ uint8_t ldv(const uint8_t *p) { return __ldcg(p); }
+__device__ __forceinline__ void atom_add(long long *p, long long x) {
+  atomicAdd(reinterpret_cast<unsigned long long *>(p), static_cast<unsigned long long>(x));
+}
+
+// ---------------------------------------------------------------- groups
+// One vertex is processed cooperatively by a group of 1 thread, 1 warp or 1 CTA.
+// All members of a group call every collective below the same number of times.
+struct ThreadG {
+  static constexpr int size = 1;
+  __device__ int rank() const { return 0; }
+  __device__ unsigned long long min(unsigned long long x) const { return x; }
+  __device__ long long sum(long long x) const { return x; }
+  __device__ long long bcast(long long x) const { return x; }
+  __device__ long long exscan(long long x, long long &tot) const { tot = x; return 0; }
+};
+
+struct WarpG {
+  static constexpr int size = 32;
+  int lane;
+  __device__ int rank() const { return lane; }
+  __device__ unsigned long long min(unsigned long long x) const {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      unsigned long long y = __shfl_xor_sync(0xffffffffu, x, o);
+      x = y < x ? y : x;
+    }
+    return x;
+  }
+  __device__ long long sum(long long x) const {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    return x;
+  }
+  __device__ long long bcast(long long x) const { return __shfl_sync(0xffffffffu, x, 0); }
+  __device__ long long exscan(long long x, long long &tot) const {
+    long long inc = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      long long y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    tot = __shfl_sync(0xffffffffu, inc, 31);
+    return inc - x;
+  }
+};
+
+// CTA group: needs WPB+1 long longs of shared scratch.
+struct BlockG {
+  static constexpr int size = NT;
+  long long *sm;   // shared scratch
+  __device__ int rank() const { return threadIdx.x; }
+  __device__ unsigned long long min(unsigned long long x) const {
+    WarpG w{(int)(threadIdx.x & 31)};
+    x = w.min(x);
+    if (w.lane == 0) sm[threadIdx.x >> 5] = (long long)x;
+    __syncthreads();
+    unsigned long long r = ~0ull;
+#pragma unroll 4
+    for (int i = 0; i < WPB; i++) { unsigned long long y = (unsigned long long)sm[i]; r = y < r ? y : r; }
+    __syncthreads();
+    return r;
+  }
+  __device__ long long sum(long long x) const {
+    WarpG w{(int)(threadIdx.x & 31)};
+    x = w.sum(x);
+    if (w.lane == 0) sm[threadIdx.x >> 5] = x;
+    __syncthreads();
+    long long r = 0;
+#pragma unroll 4
+    for (int i = 0; i < WPB; i++) r += sm[i];
+    __syncthreads();
+    return r;
+  }
+  __device__ long long bcast(long long x) const {
+    if (threadIdx.x == 0) sm[WPB] = x;
+    __syncthreads();
+    long long r = sm[WPB];
+    __syncthreads();
+    return r;
+  }
+  __device__ long long exscan(long long x, long long &tot) const {
+    WarpG w{(int)(threadIdx.x & 31)};
+    long long wt;
+    long long ex = w.exscan(x, wt);
+    if (w.lane == 0) sm[threadIdx.x >> 5] = wt;
+    __syncthreads();
+    long long before = 0, all = 0;
+    const int me = threadIdx.x >> 5;
+    for (int i = 0; i < WPB; i++) { long long y = sm[i]; if (i < me) before += y; all += y; }
+    __syncthreads();
+    tot = all;
+    return before + ex;
+  }
+};
+
+// Warp-aggregated append (ballot + popc + one leader atomic per warp).
+// Must be called by all 32 lanes (convergent).
+__device__ __forceinline__ void warp_append(bool pred, int32_t val, int32_t *list, int32_t *cnt) {
+  const unsigned m = __ballot_sync(0xffffffffu, pred);
+  if (m == 0) return;
+  const int lane = threadIdx.x & 31;
+  int base = 0;
+  if (lane == __ffs(m) - 1) base = atomicAdd(cnt, __popc(m));
+  base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+  if (pred) list[base + __popc(m & ((1u << lane) - 1u))] = val;
+}
+
+}  // namespace dmf
