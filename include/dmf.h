@@ -88,8 +88,15 @@ typedef struct {
     int64_t batch_entries;     /* k of the last batch */
     int64_t stage2_vertices;   /* |P| of the last push-pull stage 2 (Alg.8 l.29-34) */
     int64_t stage2_iterations;
+    int64_t rounds;            /* discharge rounds (a round = discharge + RIE over the queued vertices) */
+    int64_t activations;       /* vertices queued for the next round because a push made them active */
+    int64_t reset_vertices;    /* vertices whose heights were reset for a global relabel */
+    int64_t budget_stops;      /* discharge round sequences cut short by the work budget (-> global relabel) */
     float   device_ms;         /* device time of the last call's kernel(s), CUDA events */
-    float   reserved;
+    /* in-kernel phase clock (%globaltimer, block 0), microseconds, last call:
+     * prologue = batch validate/apply/clamp + source / S->T saturation,
+     * epilogue = P extraction, partitions, flow reduction, cut masks */
+    float   t_prologue_us, t_reset_us, t_bfs_us, t_discharge_us, t_rie_us, t_epilogue_us;
 } dmf_stats;
 
 /* Fill *opt with defaults (all zero / NULL; algo = DMF_DYN_PP). */

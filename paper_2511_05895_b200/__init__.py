@@ -44,7 +44,11 @@ class Stats(ctypes.Structure):
                 ("discharge_slots", ctypes.c_int64), ("pushes", ctypes.c_int64), ("relabels", ctypes.c_int64),
                 ("rie_slots", ctypes.c_int64), ("rie_saturations", ctypes.c_int64),
                 ("batch_entries", ctypes.c_int64), ("stage2_vertices", ctypes.c_int64),
-                ("stage2_iterations", ctypes.c_int64), ("device_ms", ctypes.c_float), ("reserved", ctypes.c_float)]
+                ("stage2_iterations", ctypes.c_int64), ("rounds", ctypes.c_int64), ("activations", ctypes.c_int64),
+                ("reset_vertices", ctypes.c_int64), ("budget_stops", ctypes.c_int64),
+                ("device_ms", ctypes.c_float), ("t_prologue_us", ctypes.c_float), ("t_reset_us", ctypes.c_float),
+                ("t_bfs_us", ctypes.c_float), ("t_discharge_us", ctypes.c_float), ("t_rie_us", ctypes.c_float),
+                ("t_epilogue_us", ctypes.c_float)]
 
 
 class DMFError(RuntimeError):
@@ -134,15 +138,19 @@ class DynMaxFlow:
         self._cbs = None
         if torch_alloc:
             dev = torch.cuda.current_device()
+            _cal, _cdel = torch.cuda.caching_allocator_alloc, torch.cuda.caching_allocator_delete
 
             def _alloc(nbytes, ctx):
                 try:
-                    return torch.cuda.caching_allocator_alloc(int(nbytes), dev, stream)
+                    return _cal(int(nbytes), dev, stream)
                 except Exception:
                     return None
 
             def _free(p, nbytes, ctx):
-                torch.cuda.caching_allocator_delete(int(p))
+                try:
+                    _cdel(int(p))
+                except Exception:
+                    pass
 
             self._cbs = (_ALLOC_T(_alloc), _FREE_T(_free))
             opt.alloc, opt.free = self._cbs
@@ -203,7 +211,7 @@ class DynMaxFlow:
     def stats(self) -> dict:
         st = Stats()
         self._check(self._L.dmf_get_stats(self._h, ctypes.byref(st)))
-        return {f: getattr(st, f) for f, _ in Stats._fields_ if f != "reserved"}
+        return {f: getattr(st, f) for f, _ in Stats._fields_}
 
     def export_state(self) -> dict:
         row_ptr = np.zeros(self.n + 1, np.int64)

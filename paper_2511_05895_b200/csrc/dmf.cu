@@ -12,6 +12,10 @@
 
 #include <cub/cub.cuh>
 
+#include <chrono>
+#include <cstdlib>
+#include <thread>
+#include <unistd.h>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -59,14 +63,17 @@ struct dmf_graph {
   int64_t S = 0, m = 0;
   int32_t *row = nullptr, *dst = nullptr, *rev = nullptr, *cap = nullptr, *res = nullptr, *rres = nullptr;
   int32_t *hp = nullptr, *hm = nullptr, *q0 = nullptr, *q1 = nullptr, *wl = nullptr, *rl = nullptr;
-  int32_t *plist = nullptr, *stamp = nullptr;
+  int32_t *plist = nullptr, *stamp = nullptr, *inq = nullptr;
   long long *e = nullptr;
   uint8_t *part = nullptr, *mask = nullptr;
   int32_t *bbuf = nullptr;   // batch staging: u, v, c, slot  (4 * bcap)
   int64_t bcap = 0;
   Ctl *ctl = nullptr;
   Ctl *hctl = nullptr;       // pinned mirror
+  int32_t *hdbg = nullptr;   // mapped pinned beacon (host view)
+  int32_t *ddbg = nullptr;   // device view
   int grid_blocks = 0;
+  double watchdog_s = 0;
   int32_t batch_id = 0;
   bool solved = false;
   int64_t flow = 0;
@@ -199,13 +206,15 @@ static Dev make_dev(dmf_graph *g) {
   d.n = g->n; d.s = g->s; d.t = g->t; d.kc = g->kc;
   d.max_iters = g->opt.max_iters > 0 ? g->opt.max_iters : (int32_t)(4LL * g->n + 64 > 0x3fffffff ? 0x3fffffff : 4LL * g->n + 64);
   d.batch_id = g->batch_id;
+  d.work_budget = g->S + 6LL * g->n;     // ~ the cost of one whole-graph global relabel
   d.S = g->S; d.k = 0;
   d.row = g->row; d.dst = g->dst; d.rev = g->rev; d.cap = g->cap; d.res = g->res; d.rres = g->rres;
   d.e = g->e; d.hp = g->hp; d.hm = g->hm; d.part = g->part;
   d.q0 = g->q0; d.q1 = g->q1;
-  d.wl0 = g->wl; d.wl1 = g->wl + g->n; d.wl2 = g->wl + 2 * (size_t)g->n;
-  d.rl = g->rl; d.plist = g->plist; d.stamp = g->stamp;
+  d.wl = g->wl; d.rl = g->rl; d.inq = g->inq;
+  d.plist = g->plist; d.stamp = g->stamp;
   d.mask = g->mask; d.ctl = g->ctl;
+  d.dbg = g->ddbg;
   return d;
 }
 
@@ -218,6 +227,22 @@ static int run_solve(dmf_graph *g, int32_t mode, const Dev &dv) {
   CK(cudaLaunchCooperativeKernel((const void *)k_solve<NT>, dim3(g->grid_blocks), dim3(NT), args, 0, g->stream));
   CK(cudaEventRecord(g->ev1, g->stream));
   CK(cudaMemcpyAsync(g->hctl, g->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, g->stream));
+  if (g->watchdog_s > 0) {             // debug watchdog: poll instead of blocking
+    auto t0 = std::chrono::steady_clock::now();
+    for (;;) {
+      cudaError_t q = cudaStreamQuery(g->stream);
+      if (q == cudaSuccess) break;
+      if (q != cudaErrorNotReady) CK(q);
+      const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      if (el > g->watchdog_s) {
+        fprintf(stderr, "[dmf watchdog] mode %d stuck %.1fs: phase=%d iter=%d round=%d lvl=%d a=%d b=%d\n", mode, el,
+                g->hdbg[0], g->hdbg[1], g->hdbg[2], g->hdbg[3], g->hdbg[4], g->hdbg[5]);
+        fflush(stderr);
+        _exit(3);
+      }
+      std::this_thread::sleep_for(std::chrono::microseconds(200));
+    }
+  }
   CK(cudaStreamSynchronize(g->stream));
   float ms = 0;
   cudaEventElapsedTime(&ms, g->ev0, g->ev1);
@@ -235,6 +260,16 @@ static int run_solve(dmf_graph *g, int32_t mode, const Dev &dv) {
   st.rie_saturations = (int64_t)c.stat[ST_RIE_SAT];
   st.stage2_vertices = (int64_t)c.stat[ST_S2_V];
   st.stage2_iterations = (int64_t)c.stat[ST_S2_ITERS];
+  st.rounds = (int64_t)c.stat[ST_ROUNDS];
+  st.activations = (int64_t)c.stat[ST_ACTIVATIONS];
+  st.reset_vertices = (int64_t)c.stat[ST_RESET_V];
+  st.budget_stops = (int64_t)c.stat[ST_BUDGET_STOPS];
+  st.t_prologue_us = c.stat[ST_T_PRO] * 1e-3f;
+  st.t_reset_us = c.stat[ST_T_RESET] * 1e-3f;
+  st.t_bfs_us = c.stat[ST_T_BFS] * 1e-3f;
+  st.t_discharge_us = c.stat[ST_T_DIS] * 1e-3f;
+  st.t_rie_us = c.stat[ST_T_RIE] * 1e-3f;
+  st.t_epilogue_us = c.stat[ST_T_EPI] * 1e-3f;
   st.batch_entries = dv.k;
   st.device_ms = ms;
   if (c.status != 0) {
@@ -365,16 +400,24 @@ int dmf_create(int32_t n, const int64_t *row_ptr, const int32_t *col, const int3
   g->mask = (uint8_t *)g->alloc(nn);
   g->q0 = (int32_t *)g->alloc(3 * nn * 4);
   g->q1 = (int32_t *)g->alloc(3 * nn * 4);
-  g->wl = (int32_t *)g->alloc(3 * nn * 4);
+  g->wl = (int32_t *)g->alloc(6 * nn * 4);
+  g->inq = (int32_t *)g->alloc(nn * 4);
   g->rl = (int32_t *)g->alloc(3 * nn * 4);
   g->plist = (int32_t *)g->alloc(nn * 4);
   g->ctl = (Ctl *)g->alloc(sizeof(Ctl));
   if (!g->row || !g->dst || !g->rev || !g->cap || !g->res || !g->rres || !g->stamp || !g->e || !g->hp || !g->hm ||
-      !g->part || !g->mask || !g->q0 || !g->q1 || !g->wl || !g->rl || !g->plist || !g->ctl) {
+      !g->part || !g->mask || !g->q0 || !g->q1 || !g->wl || !g->rl || !g->plist || !g->ctl || !g->inq) {
     fail(DMF_ENOMEM, "device allocation failed (state, S=%lld)", (long long)S);
     return bail(DMF_ENOMEM);
   }
   CKB(cudaMallocHost((void **)&g->hctl, sizeof(Ctl)));
+  if (const char *wd = getenv("DMF_WATCHDOG_S")) {
+    g->watchdog_s = atof(wd);
+    CKB(cudaHostAlloc((void **)&g->hdbg, 64, cudaHostAllocMapped));
+    memset(g->hdbg, 0, 64);
+    CKB(cudaHostGetDevicePointer((void **)&g->ddbg, g->hdbg, 0));
+  }
+  CKB(cudaMemsetAsync(g->inq, 0, nn * 4, st));
   if (S) {
     CKB(cudaMemsetAsync(err, 0, 64, st));
     k_rows<<<blocks(nn + 1), TB, 0, st>>>(n, S, ukey, g->row);
@@ -527,6 +570,7 @@ void dmf_destroy(dmf_graph *g) {
   if (g->stream) cudaStreamSynchronize(g->stream);
   g->release_all();
   if (g->hctl) cudaFreeHost(g->hctl);
+  if (g->hdbg) cudaFreeHost(g->hdbg);
   if (g->ev0) cudaEventDestroy(g->ev0);
   if (g->ev1) cudaEventDestroy(g->ev1);
   if (g->own_stream && g->stream) cudaStreamDestroy(g->stream);

@@ -19,7 +19,7 @@ constexpr int MIN_BLOCKS = 2;
 
 // Worklist degree bins: thread / warp / CTA per vertex.
 constexpr int32_t BIN0_MAX = 16;
-constexpr int32_t BIN1_MAX = 2048;
+constexpr int32_t BIN1_MAX = 512;
 
 // Entries of queues / worklists carry the track in bit 31 (vertex ids < 2^31).
 constexpr uint32_t TRACK_BIT = 0x80000000u;
@@ -37,20 +37,22 @@ enum Mode : int32_t {
 
 enum Stat : int {
   ST_ITERS, ST_LEVELS, ST_BFS_V, ST_BFS_SLOTS, ST_DIS_V, ST_DIS_SLOTS, ST_PUSHES,
-  ST_RELABELS, ST_RIE_SLOTS, ST_RIE_SAT, ST_S2_V, ST_S2_ITERS, ST_N
+  ST_RELABELS, ST_RIE_SLOTS, ST_RIE_SAT, ST_S2_V, ST_S2_ITERS, ST_ROUNDS, ST_ACTIVATIONS, ST_RESET_V, ST_BUDGET_STOPS,
+  ST_T_PRO, ST_T_RESET, ST_T_BFS, ST_T_DIS, ST_T_RIE, ST_T_EPI, ST_N
 };
 
 // Control block in device memory (zeroed by the host before every launch).
 struct Ctl {
   int32_t qc[9];        // BFS frontier counts [level % 3][degree bin]
-  int32_t wlc[3];       // active worklist counts per degree bin
-  int32_t rlc[3];       // relabelled-vertex list counts per degree bin
+  int32_t wlc[6];       // active worklist counts [round & 1][degree bin]
+  int32_t rlc[6];       // relabelled-vertex list counts [round & 1][degree bin]
   int32_t pcnt;         // |P| (push-pull stage 2 region)
   int32_t status;       // dmf_status of the call (0 = OK)
   int32_t err_entry;    // first offending batch entry
   int32_t iters;
   int32_t pad;
   long long flow;       // F
+  unsigned long long work[2];   // discharge + RIE work of the current / previous round
   unsigned long long stat[ST_N];
 };
 
@@ -65,6 +67,7 @@ struct Ctl {
 struct Dev {
   int32_t n, s, t, kc, max_iters;
   int32_t batch_id;
+  long long work_budget;     // discharge work (slots scanned) allowed between two global relabels
   int64_t S, k;
   const int32_t *__restrict__ row;
   const int32_t *__restrict__ dst;
@@ -74,15 +77,33 @@ struct Dev {
   int32_t *hp, *hm;          // h+ (push heights), h- (pull heights), in [0, n]
   uint8_t *part;             // PART_*
   int32_t *q0, *q1;          // BFS frontier ping-pong
-  int32_t *wl0, *wl1, *wl2;  // active worklists by degree bin
-  int32_t *rl;               // relabelled vertices (RemoveInvalidEdges scope, R13)
+  int32_t *wl;               // active worklists [2 rounds][3 bins][n]
+  int32_t *rl;               // relabelled vertices [3 bins][n] (RemoveInvalidEdges scope, R13)
+  int32_t *inq;              // per-vertex "queued for the next discharge round" flag
   int32_t *plist;            // region P of push-pull stage 2
   int32_t *stamp;            // per-slot batch stamp (duplicate detection)
   const int32_t *bu, *bv, *bc;  // batch entries
   int32_t *bslot;            // slot of each batch entry
   uint8_t *mask;             // cut output
   Ctl *ctl;
+  volatile int32_t *dbg;     // mapped pinned host words: progress beacon for the host watchdog
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// progress beacon: block 0 / thread 0 publishes (phase, iter, round, level, a, b)
+__device__ __forceinline__ void beacon(const Dev &d, int32_t phase, int32_t iter, int32_t round, int32_t lvl,
+                                       int32_t a = 0, int32_t b = 0) {
+  if (d.dbg && blockIdx.x == 0 && threadIdx.x == 0) {
+    d.dbg[1] = iter; d.dbg[2] = round; d.dbg[3] = lvl; d.dbg[4] = a; d.dbg[5] = b;
+    __threadfence_system();
+    d.dbg[0] = phase;
+  }
+}
 
 // ---------------------------------------------------------------- loads
 __device__ __forceinline__ int32_t ldv(const int32_t *p) { return __ldcg(p); }
