@@ -92,6 +92,7 @@ typedef struct {
     int64_t activations;       /* vertices queued for the next round because a push made them active */
     int64_t reset_vertices;    /* vertices whose heights were reset for a global relabel */
     int64_t budget_stops;      /* discharge round sequences cut short by the work budget (-> global relabel) */
+    int64_t bottom_up_levels;  /* BFS levels expanded bottom-up (direction-optimising BFS) */
     float   device_ms;         /* device time of the last call's kernel(s), CUDA events */
     /* in-kernel phase clock (%globaltimer, block 0), microseconds, last call:
      * prologue = batch validate/apply/clamp + source / S->T saturation,
@@ -154,6 +155,17 @@ int dmf_max_cut_source_side(dmf_graph *g, uint8_t *mask);
 
 /* Counters of the last call (see dmf_stats). */
 int dmf_get_stats(const dmf_graph *g, dmf_stats *out);
+
+/* Phase tracing (aux/debug): capacity > 0 allocates a device ring of `capacity`
+ * records; every later call records one record per grid phase of its kernel:
+ * {phase, iteration, level-or-round, items, extra, duration_ns} (int32 x 6) where
+ * phase is 0 prologue, 1 reset, 2 bfs level, 3 discharge round, 4 rie,
+ * 5 epilogue.  capacity = 0 disables tracing. */
+int dmf_set_trace(dmf_graph *g, int32_t capacity);
+
+/* Copy the trace of the LAST call: *count = records written; up to `capacity`
+ * records are copied to `records` (host or device, int32[6 * capacity]). */
+int dmf_get_trace(const dmf_graph *g, int32_t *records, int32_t capacity, int32_t *count);
 
 /* Sizes: *n vertices, *S slots, *m merged input edges (any may be NULL). */
 int dmf_sizes(const dmf_graph *g, int32_t *n, int64_t *S, int64_t *m);

@@ -45,7 +45,7 @@ class Stats(ctypes.Structure):
                 ("rie_slots", ctypes.c_int64), ("rie_saturations", ctypes.c_int64),
                 ("batch_entries", ctypes.c_int64), ("stage2_vertices", ctypes.c_int64),
                 ("stage2_iterations", ctypes.c_int64), ("rounds", ctypes.c_int64), ("activations", ctypes.c_int64),
-                ("reset_vertices", ctypes.c_int64), ("budget_stops", ctypes.c_int64),
+                ("reset_vertices", ctypes.c_int64), ("budget_stops", ctypes.c_int64), ("bottom_up_levels", ctypes.c_int64),
                 ("device_ms", ctypes.c_float), ("t_prologue_us", ctypes.c_float), ("t_reset_us", ctypes.c_float),
                 ("t_bfs_us", ctypes.c_float), ("t_discharge_us", ctypes.c_float), ("t_rie_us", ctypes.c_float),
                 ("t_epilogue_us", ctypes.c_float)]
@@ -81,11 +81,14 @@ def load_library():
         L.dmf_get_stats.argtypes = [P, ctypes.POINTER(Stats)]
         L.dmf_sizes.argtypes = [P, ctypes.POINTER(I32), ctypes.POINTER(I64), ctypes.POINTER(I64)]
         L.dmf_export_state.argtypes = [P, P, P, P, P, P, P]
+        L.dmf_set_trace.argtypes = [P, I32]
+        L.dmf_get_trace.argtypes = [P, P, I32, ctypes.POINTER(I32)]
         L.dmf_destroy.argtypes = [P]
         L.dmf_destroy.restype = None
         L.dmf_last_error.restype = ctypes.c_char_p
         for f in ("dmf_create", "dmf_static_solve", "dmf_apply_batch", "dmf_flow_value", "dmf_min_cut_source_side",
-                  "dmf_max_cut_source_side", "dmf_get_stats", "dmf_sizes", "dmf_export_state"):
+                  "dmf_max_cut_source_side", "dmf_get_stats", "dmf_sizes", "dmf_export_state", "dmf_set_trace",
+                  "dmf_get_trace"):
             getattr(L, f).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -212,6 +215,23 @@ class DynMaxFlow:
         st = Stats()
         self._check(self._L.dmf_get_stats(self._h, ctypes.byref(st)))
         return {f: getattr(st, f) for f, _ in Stats._fields_}
+
+    PHASES = {0: "prologue", 1: "reset", 2: "bfs", 3: "discharge", 4: "rie", 5: "epilogue"}
+
+    def set_trace(self, capacity: int = 4096):
+        self._check(self._L.dmf_set_trace(self._h, int(capacity)))
+
+    def trace(self) -> list:
+        """Per-phase records of the last call: dicts (phase, iter, sub, items, extra, us)."""
+        cnt = ctypes.c_int32()
+        self._check(self._L.dmf_get_trace(self._h, None, 0, ctypes.byref(cnt)))
+        buf = np.zeros(6 * max(cnt.value, 1), np.int32)
+        self._check(self._L.dmf_get_trace(self._h, _ptr(buf), cnt.value, ctypes.byref(cnt)))
+        out = []
+        for r in buf[:6 * cnt.value].reshape(-1, 6):
+            out.append(dict(phase=self.PHASES.get(int(r[0]), int(r[0])), iter=int(r[1]), sub=int(r[2]),
+                            items=int(r[3]), extra=int(r[4]), us=float(r[5]) * 1e-3))
+        return out
 
     def export_state(self) -> dict:
         row_ptr = np.zeros(self.n + 1, np.int64)

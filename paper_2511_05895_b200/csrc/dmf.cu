@@ -63,7 +63,8 @@ struct dmf_graph {
   int64_t S = 0, m = 0;
   int32_t *row = nullptr, *dst = nullptr, *rev = nullptr, *cap = nullptr, *res = nullptr, *rres = nullptr;
   int32_t *hp = nullptr, *hm = nullptr, *q0 = nullptr, *q1 = nullptr, *wl = nullptr, *rl = nullptr;
-  int32_t *plist = nullptr, *stamp = nullptr, *inq = nullptr;
+  int32_t *plist = nullptr, *stamp = nullptr, *inq = nullptr, *bul = nullptr;
+  long long *cq0 = nullptr, *cq1 = nullptr, *cqr = nullptr;
   long long *e = nullptr;
   uint8_t *part = nullptr, *mask = nullptr;
   int32_t *bbuf = nullptr;   // batch staging: u, v, c, slot  (4 * bcap)
@@ -71,6 +72,8 @@ struct dmf_graph {
   Ctl *ctl = nullptr;
   Ctl *hctl = nullptr;       // pinned mirror
   int32_t *hdbg = nullptr;   // mapped pinned beacon (host view)
+  int32_t *trace = nullptr;  // device trace ring (DMF_TRACE / dmf_set_trace)
+  int32_t trace_cap = 0;
   int32_t *ddbg = nullptr;   // device view
   int grid_blocks = 0;
   double watchdog_s = 0;
@@ -211,10 +214,13 @@ static Dev make_dev(dmf_graph *g) {
   d.row = g->row; d.dst = g->dst; d.rev = g->rev; d.cap = g->cap; d.res = g->res; d.rres = g->rres;
   d.e = g->e; d.hp = g->hp; d.hm = g->hm; d.part = g->part;
   d.q0 = g->q0; d.q1 = g->q1;
-  d.wl = g->wl; d.rl = g->rl; d.inq = g->inq;
+  d.wl = g->wl; d.rl = g->rl; d.inq = g->inq; d.bul = g->bul;
+  d.cq0 = g->cq0; d.cq1 = g->cq1; d.cqr = g->cqr;
   d.plist = g->plist; d.stamp = g->stamp;
   d.mask = g->mask; d.ctl = g->ctl;
   d.dbg = g->ddbg;
+  d.trace = g->trace;
+  d.trace_cap = g->trace_cap;
   return d;
 }
 
@@ -264,6 +270,7 @@ static int run_solve(dmf_graph *g, int32_t mode, const Dev &dv) {
   st.activations = (int64_t)c.stat[ST_ACTIVATIONS];
   st.reset_vertices = (int64_t)c.stat[ST_RESET_V];
   st.budget_stops = (int64_t)c.stat[ST_BUDGET_STOPS];
+  st.bottom_up_levels = (int64_t)c.stat[ST_BU_LEVELS];
   st.t_prologue_us = c.stat[ST_T_PRO] * 1e-3f;
   st.t_reset_us = c.stat[ST_T_RESET] * 1e-3f;
   st.t_bfs_us = c.stat[ST_T_BFS] * 1e-3f;
@@ -398,15 +405,20 @@ int dmf_create(int32_t n, const int64_t *row_ptr, const int32_t *col, const int3
   g->hm = (int32_t *)g->alloc(nn * 4);
   g->part = (uint8_t *)g->alloc(nn);
   g->mask = (uint8_t *)g->alloc(nn);
-  g->q0 = (int32_t *)g->alloc(3 * nn * 4);
-  g->q1 = (int32_t *)g->alloc(3 * nn * 4);
-  g->wl = (int32_t *)g->alloc(6 * nn * 4);
+  g->q0 = (int32_t *)g->alloc(NB * nn * 4);
+  g->q1 = (int32_t *)g->alloc(NB * nn * 4);
+  g->wl = (int32_t *)g->alloc(2 * NB * nn * 4);
   g->inq = (int32_t *)g->alloc(nn * 4);
-  g->rl = (int32_t *)g->alloc(3 * nn * 4);
+  g->bul = (int32_t *)g->alloc(2 * nn * 4);
+  const size_t cqn = (size_t)(S / CH) + nn + 64;   // >= sum over vertices of ceil(deg / CH)
+  g->cq0 = (long long *)g->alloc(cqn * 8);
+  g->cq1 = (long long *)g->alloc(cqn * 8);
+  g->cqr = (long long *)g->alloc(cqn * 8);
+  g->rl = (int32_t *)g->alloc(NB * nn * 4);
   g->plist = (int32_t *)g->alloc(nn * 4);
   g->ctl = (Ctl *)g->alloc(sizeof(Ctl));
   if (!g->row || !g->dst || !g->rev || !g->cap || !g->res || !g->rres || !g->stamp || !g->e || !g->hp || !g->hm ||
-      !g->part || !g->mask || !g->q0 || !g->q1 || !g->wl || !g->rl || !g->plist || !g->ctl || !g->inq) {
+      !g->part || !g->mask || !g->q0 || !g->q1 || !g->wl || !g->rl || !g->plist || !g->ctl || !g->inq || !g->bul || !g->cq0 || !g->cq1 || !g->cqr) {
     fail(DMF_ENOMEM, "device allocation failed (state, S=%lld)", (long long)S);
     return bail(DMF_ENOMEM);
   }
@@ -528,6 +540,30 @@ static int cut_query(dmf_graph *g, uint8_t *mask, int32_t mode) {
 
 int dmf_min_cut_source_side(dmf_graph *g, uint8_t *mask) { return cut_query(g, mask, MODE_MINCUT); }
 int dmf_max_cut_source_side(dmf_graph *g, uint8_t *mask) { return cut_query(g, mask, MODE_MAXCUT); }
+
+int dmf_set_trace(dmf_graph *g, int32_t capacity) {
+  g_last_error.clear();
+  if (!g || capacity < 0) return fail(DMF_EINVAL, "bad arguments");
+  if (g->trace) { g->release(g->trace); g->trace = nullptr; g->trace_cap = 0; }
+  if (capacity > 0) {
+    g->trace = (int32_t *)g->alloc((size_t)capacity * 6 * sizeof(int32_t));
+    if (!g->trace) return fail(DMF_ENOMEM, "trace buffer allocation failed");
+    g->trace_cap = capacity;
+  }
+  return DMF_OK;
+}
+
+int dmf_get_trace(const dmf_graph *g, int32_t *records, int32_t capacity, int32_t *count) {
+  g_last_error.clear();
+  if (!g || !count) return fail(DMF_EINVAL, "bad arguments");
+  const int32_t nrec = g->trace ? (g->hctl->ntrace < g->trace_cap ? g->hctl->ntrace : g->trace_cap) : 0;
+  *count = nrec;
+  if (records && nrec) {
+    const int32_t c = nrec < capacity ? nrec : capacity;
+    CK(cudaMemcpy(records, g->trace, (size_t)c * 6 * sizeof(int32_t), cudaMemcpyDefault));
+  }
+  return DMF_OK;
+}
 
 int dmf_get_stats(const dmf_graph *g, dmf_stats *out) {
   if (!g || !out) return fail(DMF_EINVAL, "NULL argument");

@@ -17,9 +17,12 @@ constexpr int NT = 512;
 constexpr int WPB = NT / 32;
 constexpr int MIN_BLOCKS = 2;
 
-// Worklist degree bins: thread / warp / CTA per vertex.
+// Worklist degree bins: thread / warp / CTA per vertex, and a
+// "huge" bin whose rows are split over the whole grid where the phase allows it.
+constexpr int NB = 4;
 constexpr int32_t BIN0_MAX = 16;
 constexpr int32_t BIN1_MAX = 512;
+constexpr int32_t BIN2_MAX = 8192;
 
 // Entries of queues / worklists carry the track in bit 31 (vertex ids < 2^31).
 constexpr uint32_t TRACK_BIT = 0x80000000u;
@@ -37,22 +40,26 @@ enum Mode : int32_t {
 
 enum Stat : int {
   ST_ITERS, ST_LEVELS, ST_BFS_V, ST_BFS_SLOTS, ST_DIS_V, ST_DIS_SLOTS, ST_PUSHES,
-  ST_RELABELS, ST_RIE_SLOTS, ST_RIE_SAT, ST_S2_V, ST_S2_ITERS, ST_ROUNDS, ST_ACTIVATIONS, ST_RESET_V, ST_BUDGET_STOPS,
+  ST_RELABELS, ST_RIE_SLOTS, ST_RIE_SAT, ST_S2_V, ST_S2_ITERS, ST_ROUNDS, ST_ACTIVATIONS, ST_RESET_V, ST_BUDGET_STOPS, ST_BU_LEVELS,
   ST_T_PRO, ST_T_RESET, ST_T_BFS, ST_T_DIS, ST_T_RIE, ST_T_EPI, ST_N
 };
 
 // Control block in device memory (zeroed by the host before every launch).
 struct Ctl {
-  int32_t qc[9];        // BFS frontier counts [level % 3][degree bin]
-  int32_t wlc[6];       // active worklist counts [round & 1][degree bin]
-  int32_t rlc[6];       // relabelled-vertex list counts [round & 1][degree bin]
+  int32_t qc[3 * NB];   // BFS frontier counts [level % 3][degree bin]
+  int32_t wlc[2 * NB];  // active worklist counts [round & 1][degree bin]
+  int32_t rlc[2 * NB];  // relabelled-vertex list counts [round & 1][degree bin]
   int32_t pcnt;         // |P| (push-pull stage 2 region)
+  int32_t ntrace;       // trace records written
   int32_t status;       // dmf_status of the call (0 = OK)
   int32_t err_entry;    // first offending batch entry
   int32_t iters;
   int32_t pad;
   long long flow;       // F
   unsigned long long work[2];   // discharge + RIE work of the current / previous round
+  unsigned long long fs[6];     // frontier slot counts [level % 3][track] (direction-optimising BFS)
+  int32_t bulc[4];              // bottom-up candidate queue counts [level & 1][warp/CTA bin]
+  unsigned long long mu[2];     // slots of the still-unlabelled vertices per track (BFS direction choice)
   unsigned long long stat[ST_N];
 };
 
@@ -77,9 +84,11 @@ struct Dev {
   int32_t *hp, *hm;          // h+ (push heights), h- (pull heights), in [0, n]
   uint8_t *part;             // PART_*
   int32_t *q0, *q1;          // BFS frontier ping-pong
-  int32_t *wl;               // active worklists [2 rounds][3 bins][n]
-  int32_t *rl;               // relabelled vertices [3 bins][n] (RemoveInvalidEdges scope, R13)
+  int32_t *wl;               // active worklists [2 rounds][NB bins][n]
+  int32_t *rl;               // relabelled vertices [NB bins][n] (RemoveInvalidEdges scope, R13)
   int32_t *inq;              // per-vertex "queued for the next discharge round" flag
+  int32_t *bul;              // bottom-up candidate queue [2 bins][n]
+  long long *cq0, *cq1, *cqr; // chunk queues of the frontier ping-pong and of the relabelled list
   int32_t *plist;            // region P of push-pull stage 2
   int32_t *stamp;            // per-slot batch stamp (duplicate detection)
   const int32_t *bu, *bv, *bc;  // batch entries
@@ -87,6 +96,8 @@ struct Dev {
   uint8_t *mask;             // cut output
   Ctl *ctl;
   volatile int32_t *dbg;     // mapped pinned host words: progress beacon for the host watchdog
+  int32_t *trace;            // per-phase trace records (6 ints each), NULL unless tracing
+  int32_t trace_cap;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -123,6 +134,7 @@ struct ThreadG {
   __device__ long long sum(long long x) const { return x; }
   __device__ long long bcast(long long x) const { return x; }
   __device__ long long exscan(long long x, long long &tot) const { tot = x; return 0; }
+  __device__ bool any(bool p) const { return p; }
 };
 
 struct WarpG {
@@ -143,6 +155,7 @@ struct WarpG {
     return x;
   }
   __device__ long long bcast(long long x) const { return __shfl_sync(0xffffffffu, x, 0); }
+  __device__ bool any(bool p) const { return __any_sync(0xffffffffu, p); }
   __device__ long long exscan(long long x, long long &tot) const {
     long long inc = x;
 #pragma unroll
@@ -182,6 +195,7 @@ struct BlockG {
     __syncthreads();
     return r;
   }
+  __device__ bool any(bool p) const { return __syncthreads_or(p) != 0; }
   __device__ long long bcast(long long x) const {
     if (threadIdx.x == 0) sm[WPB] = x;
     __syncthreads();

@@ -37,9 +37,15 @@ namespace dmf {
 
 constexpr int MAX_ROUNDS = 4096;  // hard cap of discharge rounds per global relabel
 
+struct TileSm {
+  int32_t cnt[8];
+  int32_t base[8];
+};
+
 struct Smem {
   long long red[WPB + 1];
   unsigned long long stat[ST_N];
+  TileSm ts;
 };
 
 // Phase clock (block 0, thread 0): time between consecutive grid barriers is
@@ -47,7 +53,8 @@ struct Smem {
 struct PhaseClock {
   unsigned long long t;
   __device__ void start() { if (blockIdx.x == 0 && threadIdx.x == 0) t = gtimer(); }
-  __device__ void lap(Smem &sm, int which);
+  __device__ void lap(const Dev &d, Smem &sm, int which, int32_t it = 0, int32_t sub = 0, int32_t items = 0,
+                      int32_t extra = 0);
 };
 
 struct Track {
@@ -70,47 +77,87 @@ __device__ __forceinline__ void sstat_add(Smem &sm, int which, unsigned long lon
   if (x) atomicAdd(&sm.stat[which], x);
 }
 
-__device__ void PhaseClock::lap(Smem &sm, int which) {
+__device__ void PhaseClock::lap(const Dev &d, Smem &sm, int which, int32_t it, int32_t sub, int32_t items,
+                                int32_t extra) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     const unsigned long long now = gtimer();
     sm.stat[which] += now - t;
+    if (d.trace && d.ctl->ntrace < d.trace_cap) {       // per-phase trace record (DMF_TRACE)
+      int32_t *rec = d.trace + 6 * d.ctl->ntrace++;
+      rec[0] = which - ST_T_PRO; rec[1] = it; rec[2] = sub; rec[3] = items; rec[4] = extra; rec[5] = (int32_t)(now - t);
+    }
     t = now;
   }
 }
 
 __device__ __forceinline__ int bin_of(const Dev &d, int32_t v) {
   const int32_t deg = d.row[v + 1] - d.row[v];
-  return deg <= BIN0_MAX ? 0 : (deg <= BIN1_MAX ? 1 : 2);
+  return deg <= BIN0_MAX ? 0 : (deg <= BIN1_MAX ? 1 : (deg <= BIN2_MAX ? 2 : 3));
 }
 
-// Binned list view: three buffers (n entries each) and three counters.
+// Binned list view: NB buffers (n entries each) and NB counters.  A CHUNKED list
+// (BFS frontiers, relabelled lists: phases whose per-slot work is independent)
+// stores every vertex of more than BIN1_MAX slots as ceil(deg/CH) (vertex, chunk)
+// entries in `cq` (count in c[3]), so that one warp takes one CH-slot chunk and
+// hub rows are spread over the whole grid (edge-balanced work units).
+constexpr int32_t CH = 512;
+
 struct BL {
   int32_t *buf;   // bin b at buf + b*n
   int32_t *c;
   int32_t n;
+  long long *cq;  // chunk queue (nullptr: not chunked)
   __device__ int32_t *bin(int b) const { return buf + (size_t)b * n; }
 };
 
+__device__ __forceinline__ long long chunk_entry(int32_t v, uint32_t tag, int32_t k) {
+  return ((long long)k << 32) | (long long)((uint32_t)v | tag);
+}
+
 // append v (with track tag) to its degree bin; convergent (whole warp) or not
 __device__ __forceinline__ void bl_append_conv(const Dev &d, const BL &bl, bool pred, int32_t v, uint32_t tag) {
-  const int bin = pred ? bin_of(d, v) : -1;
-#pragma unroll
-  for (int b = 0; b < 3; b++) warp_append(pred && bin == b, (int32_t)((uint32_t)v | tag), bl.bin(b), bl.c + b);
+  const int32_t deg = pred ? d.row[v + 1] - d.row[v] : 0;
+  const int bin = !pred ? -1 : (deg <= BIN0_MAX ? 0 : (deg <= BIN1_MAX ? 1 : (deg <= BIN2_MAX ? 2 : 3)));
+  warp_append(bin == 0, (int32_t)((uint32_t)v | tag), bl.bin(0), bl.c);
+  warp_append(bin == 1, (int32_t)((uint32_t)v | tag), bl.bin(1), bl.c + 1);
+  if (bl.cq) {
+    const int32_t nch = bin >= 2 ? (deg + CH - 1) / CH : 0;
+    if (__ballot_sync(0xffffffffu, nch > 0) == 0) return;
+    WarpG g{(int)(threadIdx.x & 31)};
+    long long tot;
+    const int32_t ex = (int32_t)g.exscan(nch, tot);
+    int32_t base = 0;
+    if (g.lane == 0) base = atomicAdd(bl.c + 3, (int32_t)tot);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    for (int32_t k = 0; k < nch; k++) bl.cq[base + ex + k] = chunk_entry(v, tag, k);
+  } else {
+    warp_append(bin == 2, (int32_t)((uint32_t)v | tag), bl.bin(2), bl.c + 2);
+    warp_append(bin == 3, (int32_t)((uint32_t)v | tag), bl.bin(3), bl.c + 3);
+  }
 }
 __device__ __forceinline__ void bl_append_one(const Dev &d, const BL &bl, int32_t v, uint32_t tag) {
-  const int bin = bin_of(d, v);
+  const int32_t deg = d.row[v + 1] - d.row[v];
+  const int bin = deg <= BIN0_MAX ? 0 : (deg <= BIN1_MAX ? 1 : (deg <= BIN2_MAX ? 2 : 3));
+  if (bin >= 2 && bl.cq) {
+    const int32_t nch = (deg + CH - 1) / CH;
+    const int32_t pos = atomicAdd(bl.c + 3, nch);
+    for (int32_t k = 0; k < nch; k++) bl.cq[pos + k] = chunk_entry(v, tag, k);
+    return;
+  }
   const int pos = atomicAdd(bl.c + bin, 1);
   bl.bin(bin)[pos] = (int32_t)((uint32_t)v | tag);
 }
 
-// Process a binned list: CTA per bin-2 entry, warp per bin-1 entry, thread per
-// bin-0 entry.  fn(group, entry).
+// Process a binned list: CTA per bin-3 / bin-2 entry, warp per bin-1 entry, thread
+// per bin-0 entry.  fn(group, entry).
 template <class Fn>
-__device__ __forceinline__ void process_bl(const BL &bl, const int32_t c[3], Smem &sm, Fn fn) {
+__device__ __forceinline__ void process_bl(const BL &bl, const int32_t c[NB], Smem &sm, Fn fn) {
   {
     BlockG g{sm.red};
-    const int32_t *b = bl.bin(2);
-    for (int32_t x = blockIdx.x; x < c[2]; x += gridDim.x) fn(g, b[x]);
+    for (int b = 3; b >= 2; b--) {
+      const int32_t *lst = bl.bin(b);
+      for (int32_t x = blockIdx.x; x < c[b]; x += gridDim.x) fn(g, lst[x]);
+    }
   }
   {
     WarpG g{(int)(threadIdx.x & 31)};
@@ -126,6 +173,17 @@ __device__ __forceinline__ void process_bl(const BL &bl, const int32_t c[3], Sme
   }
 }
 
+__device__ __forceinline__ void read_counts(const int32_t *p, int32_t c[NB]) {
+#pragma unroll
+  for (int b = 0; b < NB; b++) c[b] = ldv(p + b);
+}
+__device__ __forceinline__ int32_t total(const int32_t c[NB]) {
+  int32_t t = 0;
+#pragma unroll
+  for (int b = 0; b < NB; b++) t += c[b];
+  return t;
+}
+
 // Queue a vertex whose excess (track-signed) just crossed from <= 0 to > 0 for the
 // next discharge round, at most once per round (inq flag).
 __device__ __forceinline__ void activate(const Dev &d, const Track &k, const BL &nxt, int32_t v, uint32_t tag,
@@ -138,66 +196,142 @@ __device__ __forceinline__ void activate(const Dev &d, const Track &k, const BL 
 }
 
 // ---------------------------------------------------------------------------
-// BFS: one residual slot i scanned from frontier vertex w at level lvl.  A residual
-// edge (v -> w) [push track] / (w -> v) [pull track] lets v be labelled lvl+1.
+// BFS (global relabel).  Level-synchronous; per level and per
+// track it is either
+//   top-down   the frontier's rows are scanned: a residual edge (v -> w) [push
+//              track] / (w -> v) [pull track] from frontier vertex w labels v, or
+//   bottom-up  every unlabelled vertex of the track's region looks for a residual
+//              edge into the frontier and stops at the first (direction-optimising
+//              BFS; chosen when the frontier's slots exceed 1/BU_ALPHA of the
+//              unlabelled vertices' slots).
+// and the next frontier / active worklist are built either
+//   SPARSE     claims by CAS and warp-aggregated appends inside the expansion (small
+//              frontiers: little contention), or
+//   DENSE      labels are plain idempotent stores h(v) = lvl+1 and a separate tiled
+//              compaction over the vertex domain builds the next frontier and the
+//              worklist with block-aggregated appends (ballot + one global atomic per
+//              list per 2048-vertex tile -- the paper's ballot worklist).
+constexpr unsigned long long BU_ALPHA = 2;
+constexpr unsigned long long SPARSE_DIV = 64;     // sparse iff frontier slots < S / SPARSE_DIV
+constexpr int TILE_ITEMS = 4;                     // vertices per thread per compaction tile
+
 struct BfsCtx {
   int32_t lvl;
   uint8_t reg0, reg1;
   bool collect;
+  bool bu[2];                       // bottom-up this level, per track
+  bool sparse;                      // CAS + appends in the expansion
   BL next, wl;
+  unsigned long long *fs_next;      // [2] slot counts of the next frontier per track
 };
 
-__device__ __forceinline__ void bfs_slot(const Dev &d, const BfsCtx &c, int tr, int32_t i, bool valid,
-                                         bool &claimed, bool &act, int32_t &v) {
-  claimed = false; act = false; v = -1;
-  if (!valid) return;
-  const Track k = make_track(d, tr);
-  const int32_t rb = ldv(k.B + i);
-  const int32_t vv = d.dst[i];
-  if (rb <= 0) return;
-  v = vv;
-  const uint8_t reg = tr ? c.reg1 : c.reg0;
-  if (v == k.excl || ldv(k.hgt + v) != d.n) return;
-  if (reg != 0 && ldv(d.part + v) != reg) return;
-  claimed = atomicCAS(k.hgt + v, d.n, c.lvl + 1) == d.n;
-  if (claimed && c.collect) {
-    const long long ev = ldv(d.e + v);
-    act = tr ? (ev < 0) : (ev > 0);
+// ---- SPARSE claims -----------------------------------------------------------
+__device__ __forceinline__ void claim_append(const Dev &d, const BfsCtx &c, bool claimed, bool act, int32_t v, int tr) {
+  bl_append_conv(d, c.next, claimed && tr == 0, v, 0u);
+  bl_append_conv(d, c.next, claimed && tr == 1, v, TRACK_BIT);
+  if (c.collect) {
+    bl_append_conv(d, c.wl, act && tr == 0, v, 0u);
+    bl_append_conv(d, c.wl, act && tr == 1, v, TRACK_BIT);
+  }
+  const unsigned m = __ballot_sync(0xffffffffu, claimed);
+  if (m) {
+    const long long deg = claimed ? (long long)(d.row[v + 1] - d.row[v]) : 0;
+    WarpG g{(int)(threadIdx.x & 31)};
+    const long long d0 = g.sum(tr == 0 ? deg : 0), d1 = g.sum(tr == 1 ? deg : 0);
+    if (g.lane == 0) {
+      if (d0) atomicAdd(c.fs_next, (unsigned long long)d0);
+      if (d1) atomicAdd(c.fs_next + 1, (unsigned long long)d1);
+    }
   }
 }
 
-// warp (or CTA) per frontier vertex: coalesced scan of its row
-template <class G>
-__device__ __forceinline__ void bfs_expand_group(const Dev &d, const G &g, Smem &sm, int32_t entry, const BfsCtx &c) {
-  const int tr = ((uint32_t)entry & TRACK_BIT) ? 1 : 0;
-  const int32_t w = (int32_t)((uint32_t)entry & ~TRACK_BIT);
-  const uint32_t tag = tr ? TRACK_BIT : 0u;
-  const int32_t beg = d.row[w], end = d.row[w + 1];
-  for (int32_t base = beg; base < end; base += G::size) {
-    const int32_t i = base + g.rank();
-    bool claimed, act;
-    int32_t v;
-    bfs_slot(d, c, tr, i, i < end, claimed, act, v);
-    bl_append_conv(d, c.next, claimed, v, tag);
-    if (c.collect) bl_append_conv(d, c.wl, act, v, tag);
+// one scanned slot (rb = the track's BFS residual, v = head); warp-convergent
+__device__ __forceinline__ void td_slot(const Dev &d, const BfsCtx &c, int tr, int32_t rb, int32_t v) {
+  const Track k = make_track(d, tr);
+  const uint8_t reg = tr ? c.reg1 : c.reg0;
+  bool ok = false;
+  if (rb > 0 && v != k.excl) {
+    const int32_t h = ldv(k.hgt + v);
+    const uint8_t p = reg ? ldv(d.part + v) : 0;       // issued together with h
+    ok = h == d.n && (reg == 0 || p == reg);
   }
-  if (g.rank() == 0) {
+  if (c.sparse) {
+    bool claimed = false, act = false;
+    if (ok) {
+      claimed = atomicCAS(k.hgt + v, d.n, c.lvl + 1) == d.n;
+      if (claimed && c.collect) {
+        const long long ev = ldv(d.e + v);
+        act = tr ? (ev < 0) : (ev > 0);
+      }
+    }
+    claim_append(d, c, claimed, act, v, tr);
+  } else if (ok) {
+    k.hgt[v] = c.lvl + 1;                              // idempotent: every writer writes lvl+1
+  }
+}
+
+// warp per frontier vertex (bin 1): coalesced scan of its row, 4 slots per lane per step
+__device__ __forceinline__ void td_vertex_warp(const Dev &d, Smem &sm, int32_t entry, const BfsCtx &c) {
+  const int tr = ((uint32_t)entry & TRACK_BIT) ? 1 : 0;
+  if (c.bu[tr]) return;
+  const int lane = threadIdx.x & 31;
+  const int32_t w = (int32_t)((uint32_t)entry & ~TRACK_BIT);
+  const int32_t beg = d.row[w], end = d.row[w + 1];
+  const int32_t *B = make_track(d, tr).B;
+  for (int32_t base = beg; base < end; base += 128) {
+    int32_t rb[4], vv[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const int32_t i = base + j * 32 + lane;
+      rb[j] = i < end ? ldv(B + i) : 0;
+      vv[j] = i < end ? d.dst[i] : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; j++) td_slot(d, c, tr, rb[j], vv[j]);
+  }
+  if (lane == 0) {
     sstat_add(sm, ST_BFS_SLOTS, (unsigned long long)(end - beg));
     sstat_add(sm, ST_BFS_V, 1);
   }
 }
 
-// warp over a chunk of up to 32 low-degree frontier vertices: the concatenation of
-// their rows is split evenly over the lanes (degree exclusive scan + shuffle search)
-__device__ __forceinline__ void bfs_expand_chunk(const Dev &d, Smem &sm, const int32_t *list, int32_t x0,
-                                                 int32_t cnt, const BfsCtx &c) {
+// warp per CH-slot chunk of a big frontier row (edge-balanced)
+__device__ __forceinline__ void td_chunk_warp(const Dev &d, Smem &sm, long long ce, const BfsCtx &c) {
+  const uint32_t lo = (uint32_t)ce;
+  const int tr = (lo & TRACK_BIT) ? 1 : 0;
+  if (c.bu[tr]) return;
+  const int lane = threadIdx.x & 31;
+  const int32_t w = (int32_t)(lo & ~TRACK_BIT);
+  const int32_t rb0 = d.row[w] + (int32_t)(ce >> 32) * CH;
+  const int32_t end = min(d.row[w + 1], rb0 + CH);
+  const int32_t *B = make_track(d, tr).B;
+  for (int32_t base = rb0; base < end; base += 128) {
+    int32_t rb[4], vv[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const int32_t i = base + j * 32 + lane;
+      rb[j] = i < end ? ldv(B + i) : 0;
+      vv[j] = i < end ? d.dst[i] : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; j++) td_slot(d, c, tr, rb[j], vv[j]);
+  }
+  if (lane == 0) sstat_add(sm, ST_BFS_SLOTS, (unsigned long long)(end - rb0));
+}
+
+// warp over up to 32 low-degree frontier vertices (bin 0): their rows are
+// concatenated and split evenly over the lanes (degree scan + shuffle search)
+__device__ __forceinline__ void td_small_chunk(const Dev &d, Smem &sm, const int32_t *list, int32_t x0, int32_t cnt,
+                                               const BfsCtx &c) {
   const int lane = threadIdx.x & 31;
   int32_t entry = 0, beg = 0, deg = 0;
   if (lane < cnt) {
     entry = list[x0 + lane];
     const int32_t w = (int32_t)((uint32_t)entry & ~TRACK_BIT);
-    beg = d.row[w];
-    deg = d.row[w + 1] - beg;
+    if (!c.bu[((uint32_t)entry & TRACK_BIT) ? 1 : 0]) {
+      beg = d.row[w];
+      deg = d.row[w + 1] - beg;
+    }
   }
   WarpG g{lane};
   long long tot;
@@ -215,16 +349,10 @@ __device__ __forceinline__ void bfs_expand_chunk(const Dev &d, Smem &sm, const i
     const int32_t bj = __shfl_sync(0xffffffffu, beg, j);
     const int32_t oj = __shfl_sync(0xffffffffu, off, j);
     const int tr = ((uint32_t)ej & TRACK_BIT) ? 1 : 0;
-    bool claimed, act;
-    int32_t v;
-    bfs_slot(d, c, tr, bj + (k - oj), k < total, claimed, act, v);
-    // tracks may differ between lanes: append per tag
-    bl_append_conv(d, c.next, claimed && tr == 0, v, 0u);
-    bl_append_conv(d, c.next, claimed && tr == 1, v, TRACK_BIT);
-    if (c.collect) {
-      bl_append_conv(d, c.wl, act && tr == 0, v, 0u);
-      bl_append_conv(d, c.wl, act && tr == 1, v, TRACK_BIT);
-    }
+    const int32_t i = bj + (k - oj);
+    int32_t rb = 0, v = 0;
+    if (k < total) { rb = ldv(make_track(d, tr).B + i); v = d.dst[i]; }
+    td_slot(d, c, tr, rb, v);
   }
   if (lane == 0) {
     sstat_add(sm, ST_BFS_SLOTS, (unsigned long long)total);
@@ -232,21 +360,208 @@ __device__ __forceinline__ void bfs_expand_chunk(const Dev &d, Smem &sm, const i
   }
 }
 
-__device__ __forceinline__ void bfs_level(const Dev &d, Smem &sm, const BL &cur, const int32_t c[3], const BfsCtx &ctx) {
-  {
-    BlockG g{sm.red};
-    const int32_t *b = cur.bin(2);
-    for (int32_t x = blockIdx.x; x < c[2]; x += gridDim.x) bfs_expand_group(d, g, sm, b[x], ctx);
+// ---- bottom-up ----------------------------------------------------------------
+// Pass A (thread per vertex) settles low-degree candidates and queues the others
+// (degree-binned); pass B (after a grid barrier) scans the queued rows with a
+// warp / a CTA per vertex and group-wide early exit.  Labels are stores.
+constexpr int32_t BU_THREAD_MAX = 16;
+
+__device__ __forceinline__ int bu_candidate(const Dev &d, const BfsCtx &c, int32_t v) {
+  if (c.bu[0] && v != d.s && ldv(d.hp + v) == d.n && (c.reg0 == 0 || ldv(d.part + v) == c.reg0)) return 0;
+  if (c.bu[1] && v != d.t && ldv(d.hm + v) == d.n && (c.reg1 == 0 || ldv(d.part + v) == c.reg1)) return 1;
+  return -1;
+}
+
+__device__ __forceinline__ void bfs_bottom_up_a(const Dev &d, Smem &sm, const BfsCtx &c, int32_t *bul, int32_t *bulc) {
+  const int32_t n = d.n;
+  const int32_t nt = gridDim.x * NT;
+  unsigned long long scanned = 0;
+  for (int32_t b = blockIdx.x * NT + (threadIdx.x & ~31); b < n; b += nt) {
+    const int32_t v = b + (threadIdx.x & 31);
+    bool q1 = false, q2 = false;
+    int tr = 0;
+    if (v < n) {
+      const int cand = bu_candidate(d, c, v);
+      if (cand >= 0) {
+        tr = cand;
+        const int32_t beg = d.row[v], end = d.row[v + 1];
+        if (end - beg > BU_THREAD_MAX) {
+          q1 = end - beg <= BIN1_MAX;
+          q2 = !q1;
+        } else {
+          const Track k = make_track(d, tr);
+          bool hit = false;
+          for (int32_t i0 = beg; i0 < end && !hit; i0 += 4) {
+            int32_t r[4], w[4];
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+              r[j] = i0 + j < end ? ldv(k.F + i0 + j) : 0;
+              w[j] = i0 + j < end ? d.dst[i0 + j] : 0;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; j++)
+              if (!hit && r[j] > 0 && ldv(k.hgt + w[j]) == c.lvl) hit = true;
+            scanned += 4;
+          }
+          if (hit) k.hgt[v] = c.lvl + 1;
+        }
+      }
+    }
+    const uint32_t tag = tr ? TRACK_BIT : 0u;
+    warp_append(q1, (int32_t)((uint32_t)v | tag), bul, bulc);
+    warp_append(q2, (int32_t)((uint32_t)v | tag), bul + n, bulc + 1);
   }
-  const int32_t gw = blockIdx.x * WPB + (threadIdx.x >> 5), nw = gridDim.x * WPB;
-  {
-    WarpG g{(int)(threadIdx.x & 31)};
-    const int32_t *b = cur.bin(1);
-    for (int32_t x = gw; x < c[1]; x += nw) bfs_expand_group(d, g, sm, b[x], ctx);
+  sstat_add(sm, ST_BFS_SLOTS, scanned);
+}
+
+template <class G>
+__device__ __forceinline__ void bfs_bottom_up_b(const Dev &d, const G &g, Smem &sm, const BfsCtx &c, int32_t entry) {
+  const int tr = ((uint32_t)entry & TRACK_BIT) ? 1 : 0;
+  const int32_t v = (int32_t)((uint32_t)entry & ~TRACK_BIT);
+  const Track k = make_track(d, tr);
+  const int32_t beg = d.row[v], end = d.row[v + 1];
+  bool found = false;
+  unsigned long long scanned = 0;
+  for (int32_t base = beg; base < end; base += 4 * G::size) {
+    int32_t r[4], w[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const int32_t i = base + j * G::size + g.rank();
+      r[j] = i < end ? ldv(k.F + i) : 0;
+      w[j] = i < end ? d.dst[i] : 0;
+    }
+    bool hit = false;
+#pragma unroll
+    for (int j = 0; j < 4; j++)
+      if (r[j] > 0 && ldv(k.hgt + w[j]) == c.lvl) hit = true;
+    scanned += 4 * G::size;
+    if (g.any(hit)) { found = true; break; }
   }
-  {
-    const int32_t *b = cur.bin(0);
-    for (int32_t x = gw * 32; x < c[0]; x += nw * 32) bfs_expand_chunk(d, sm, b, x, min(32, c[0] - x), ctx);
+  if (g.rank() == 0) {
+    if (found) k.hgt[v] = c.lvl + 1;
+    sstat_add(sm, ST_BFS_SLOTS, scanned);
+  }
+}
+
+// ---- DENSE compaction ---------------------------------------------------------
+// Tiled pass over the vertex domain (all n, or the P list): every thread classifies
+// TILE_ITEMS vertices; per tile, warps reserve positions with shared-memory atomics
+// and thread 0 reserves each list's global range with ONE atomic.  Categories:
+// 0,1 = frontier bins 0/1, 2 = frontier chunks (several entries per vertex),
+// 3..6 = worklist bins 0..3.  `classify(v, tr, front, act)` decides for vertex v.
+template <class Classify>
+__device__ __forceinline__ void compact_domain(const Dev &d, TileSm &ts, int32_t N, const int32_t *dom,
+                                               const BL &next, const BL &wl, bool collect, Classify classify,
+                                               long long &fs0, long long &fs1) {
+  const int lane = threadIdx.x & 31;
+  const int32_t tile_sz = TILE_ITEMS * NT;
+  WarpG g{lane};
+  int32_t *gcnt[7] = {next.c, next.c + 1, next.c + 3, wl.c, wl.c + 1, wl.c + 2, wl.c + 3};
+  for (int32_t t0 = blockIdx.x * tile_sz; t0 < N; t0 += gridDim.x * tile_sz) {
+    if (threadIdx.x < 8) ts.cnt[threadIdx.x] = 0;
+    __syncthreads();
+    int32_t vv[TILE_ITEMS], fo[TILE_ITEMS], wo[TILE_ITEMS];
+    int8_t fc[TILE_ITEMS], wc[TILE_ITEMS];
+    uint32_t tg[TILE_ITEMS];
+    int32_t nchv[TILE_ITEMS];
+#pragma unroll
+    for (int j = 0; j < TILE_ITEMS; j++) {
+      const int32_t x = t0 + j * NT + threadIdx.x;
+      int32_t v = -1;
+      int tr = 0;
+      bool front = false, act = false;
+      int32_t deg = 0;
+      if (x < N) {
+        v = dom ? dom[x] : x;
+        classify(v, tr, front, act);
+        if (front || act) deg = d.row[v + 1] - d.row[v];
+      }
+      const int fb = front ? (deg <= BIN0_MAX ? 0 : (deg <= BIN1_MAX ? 1 : 2)) : -1;
+      const int wb = (collect && act) ? (deg <= BIN0_MAX ? 0 : (deg <= BIN1_MAX ? 1 : (deg <= BIN2_MAX ? 2 : 3))) : -1;
+      if (front) { if (tr) fs1 += deg; else fs0 += deg; }
+      vv[j] = v; fc[j] = (int8_t)fb; wc[j] = (int8_t)wb; tg[j] = tr ? TRACK_BIT : 0u;
+      fo[j] = 0; wo[j] = 0;
+      // frontier bins 0/1: ballot per bin
+#pragma unroll
+      for (int b = 0; b < 2; b++) {
+        const unsigned m = __ballot_sync(0xffffffffu, fb == b);
+        if (m) {
+          int bs = 0;
+          if (lane == __ffs(m) - 1) bs = atomicAdd(&ts.cnt[b], __popc(m));
+          bs = __shfl_sync(0xffffffffu, bs, __ffs(m) - 1);
+          if (fb == b) fo[j] = bs + __popc(m & ((1u << lane) - 1u));
+        }
+      }
+      // frontier chunks
+      const int32_t nch = fb == 2 ? (deg + CH - 1) / CH : 0;
+      nchv[j] = nch;
+      if (__ballot_sync(0xffffffffu, nch > 0)) {
+        long long tot;
+        const int32_t ex = (int32_t)g.exscan(nch, tot);
+        int bs = 0;
+        if (lane == 0) bs = atomicAdd(&ts.cnt[2], (int32_t)tot);
+        bs = __shfl_sync(0xffffffffu, bs, 0);
+        if (fb == 2) fo[j] = bs + ex;
+      }
+      // worklist bins
+      if (collect) {
+#pragma unroll
+        for (int b = 0; b < 4; b++) {
+          const unsigned m = __ballot_sync(0xffffffffu, wb == b);
+          if (m) {
+            int bs = 0;
+            if (lane == __ffs(m) - 1) bs = atomicAdd(&ts.cnt[3 + b], __popc(m));
+            bs = __shfl_sync(0xffffffffu, bs, __ffs(m) - 1);
+            if (wb == b) wo[j] = bs + __popc(m & ((1u << lane) - 1u));
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < 7) {
+      const int32_t cc = ts.cnt[threadIdx.x];
+      ts.base[threadIdx.x] = cc ? atomicAdd(gcnt[threadIdx.x], cc) : 0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < TILE_ITEMS; j++) {
+      const int32_t e = (int32_t)((uint32_t)vv[j] | tg[j]);
+      if (fc[j] == 0 || fc[j] == 1) next.bin(fc[j])[ts.base[fc[j]] + fo[j]] = e;
+      else if (fc[j] == 2)
+        for (int32_t k = 0; k < nchv[j]; k++) next.cq[ts.base[2] + fo[j] + k] = chunk_entry(vv[j], tg[j], k);
+      if (wc[j] >= 0) wl.bin(wc[j])[ts.base[3 + wc[j]] + wo[j]] = e;
+    }
+    __syncthreads();
+  }
+}
+
+// One BFS level (expansion; claims).  Ends after its grid barrier(s).
+__device__ __forceinline__ void bfs_expand_level(const Dev &d, cg::grid_group &grid, Smem &sm, const BL &cur,
+                                                 const int32_t c[NB], const BfsCtx &ctx, int32_t *bul, int32_t *bulc) {
+  const bool bu = ctx.bu[0] || ctx.bu[1];
+  if (bu) bfs_bottom_up_a(d, sm, ctx, bul, bulc);
+  if (!(ctx.bu[0] && ctx.bu[1])) {
+    const int32_t gw = blockIdx.x * WPB + (threadIdx.x >> 5), nw = gridDim.x * WPB;
+    for (int32_t x = gw; x < c[3]; x += nw) td_chunk_warp(d, sm, cur.cq[x], ctx);
+    for (int32_t x = gw; x < c[1]; x += nw) td_vertex_warp(d, sm, cur.bin(1)[x], ctx);
+    const int32_t *b0 = cur.bin(0);
+    for (int32_t x = gw * 32; x < c[0]; x += nw * 32) td_small_chunk(d, sm, b0, x, min(32, c[0] - x), ctx);
+  }
+  grid.sync();
+  if (bu) {
+    const int32_t q1 = ldv(bulc), q2 = ldv(bulc + 1);
+    if (q1 + q2 > 0) {
+      {
+        BlockG g{sm.red};
+        for (int32_t x = blockIdx.x; x < q2; x += gridDim.x) bfs_bottom_up_b(d, g, sm, ctx, bul[d.n + x]);
+      }
+      {
+        WarpG g{(int)(threadIdx.x & 31)};
+        const int32_t gw = blockIdx.x * WPB + (threadIdx.x >> 5), nw = gridDim.x * WPB;
+        for (int32_t x = gw; x < q1; x += nw) bfs_bottom_up_b(d, g, sm, ctx, bul[x]);
+      }
+      grid.sync();
+    }
   }
 }
 
@@ -363,18 +678,11 @@ __device__ __forceinline__ void discharge(const Dev &d, const G &g, Smem &sm, in
 // h+(u) > h+(v)+1.  Pull track: in-slots (v,u) with h-(u) > h-(v)+1 (the head is
 // the relabelled end, R13).  Heights are frozen in this phase and each residual
 // pair has one writer, so the slot stores need no atomics.
-template <class G>
-__device__ __forceinline__ void rie(const Dev &d, const G &g, Smem &sm, int32_t entry, const BL &nxt,
-                                    unsigned long long *workc) {
-  const int tr = ((uint32_t)entry & TRACK_BIT) ? 1 : 0;
-  const uint32_t tag = tr ? TRACK_BIT : 0u;
-  const int32_t u = (int32_t)((uint32_t)entry & ~TRACK_BIT);
-  const Track k = make_track(d, tr);
-  const int32_t beg = d.row[u], end = d.row[u + 1];
-  const int32_t hu = ldv(k.hgt + u);
-  long long moved = 0;
-  unsigned long long sat = 0;
-  for (int32_t i = beg + g.rank(); i < end; i += G::size) {
+// slots [i0, end) step `step` of relabelled vertex u (one thread's share)
+__device__ __forceinline__ void rie_slots(const Dev &d, const Track &k, int32_t u, int32_t hu, int32_t i0, int32_t end,
+                                          int32_t step, uint32_t tag, const BL &nxt, Smem &sm, long long &moved,
+                                          unsigned long long &sat) {
+  for (int32_t i = i0; i < end; i += step) {
     const int32_t r = ldv(k.F + i);
     if (r > 0) {
       const int32_t v = d.dst[i];
@@ -393,6 +701,20 @@ __device__ __forceinline__ void rie(const Dev &d, const G &g, Smem &sm, int32_t 
       }
     }
   }
+}
+
+template <class G>
+__device__ __forceinline__ void rie(const Dev &d, const G &g, Smem &sm, int32_t entry, const BL &nxt,
+                                    unsigned long long *workc) {
+  const int tr = ((uint32_t)entry & TRACK_BIT) ? 1 : 0;
+  const uint32_t tag = tr ? TRACK_BIT : 0u;
+  const int32_t u = (int32_t)((uint32_t)entry & ~TRACK_BIT);
+  const Track k = make_track(d, tr);
+  const int32_t beg = d.row[u], end = d.row[u + 1];
+  const int32_t hu = ldv(k.hgt + u);
+  long long moved = 0;
+  unsigned long long sat = 0;
+  rie_slots(d, k, u, hu, beg + g.rank(), end, G::size, tag, nxt, sm, moved, sat);
   moved = g.sum(moved);
   if (g.rank() == 0) {
     if (moved) atom_add(d.e + u, -moved * k.sign);
@@ -402,26 +724,60 @@ __device__ __forceinline__ void rie(const Dev &d, const G &g, Smem &sm, int32_t 
   sstat_add(sm, ST_RIE_SAT, sat);
 }
 
+// RIE of chunked relabelled entries: one warp per CH-slot piece of a big row.
+__device__ __forceinline__ void rie_chunks(const Dev &d, Smem &sm, const long long *cq, int32_t cnt, const BL &nxt,
+                                           unsigned long long *workc) {
+  const int lane = threadIdx.x & 31;
+  const int32_t gw = blockIdx.x * WPB + (threadIdx.x >> 5), nw = gridDim.x * WPB;
+  WarpG g{lane};
+  for (int32_t x = gw; x < cnt; x += nw) {
+    const long long ce = cq[x];
+    const uint32_t lo = (uint32_t)ce;
+    const int tr = (lo & TRACK_BIT) ? 1 : 0;
+    const uint32_t tag = tr ? TRACK_BIT : 0u;
+    const int32_t u = (int32_t)(lo & ~TRACK_BIT);
+    const Track k = make_track(d, tr);
+    const int32_t beg = d.row[u] + (int32_t)(ce >> 32) * CH;
+    const int32_t end = min(d.row[u + 1], beg + CH);
+    const int32_t hu = ldv(k.hgt + u);
+    long long moved = 0;
+    unsigned long long sat = 0;
+    rie_slots(d, k, u, hu, beg + lane, end, 32, tag, nxt, sm, moved, sat);
+    moved = g.sum(moved);
+    if (lane == 0) {
+      if (moved) atom_add(d.e + u, -moved * k.sign);
+      atomicAdd(workc, (unsigned long long)(end - beg));
+      sstat_add(sm, ST_RIE_SLOTS, (unsigned long long)(end - beg));
+    }
+    sstat_add(sm, ST_RIE_SAT, sat);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Roots of a global relabel.
 enum ResetKind : int { RK_PUSH = 0, RK_PP = 1, RK_STAGE2 = 2, RK_MINCUT = 3, RK_MAXCUT = 4 };
 
 struct Lists {
-  int32_t *q[2];    // frontier ping-pong, [3 bins][n] each
-  int32_t *wl[2];   // worklist ping-pong, [3 bins][n] each
-  int32_t *rl;      // relabelled, [3 bins][n]
+  int32_t *q[2];    // frontier ping-pong, [NB bins][n] each
+  long long *qc[2]; // their chunk queues
+  int32_t *wl[2];   // worklist ping-pong, [NB bins][n] each
+  int32_t *rl;      // relabelled, [NB bins][n]
+  long long *rlc;   // its chunk queue
 };
+
 
 // The device loop: repeat { RESET; BFS levels (+ worklist); if no active: stop;
 //                           rounds of { DISCHARGE; RIE } until no vertex is queued }.
 // Counter discipline (each counter is zeroed by block 0 in a phase where nobody
 // else reads or appends it, then published by the next grid barrier):
-//   qc[l%3]   appended at level l-1 (RESET for l=0), read at level l,
-//             zeroed at level l+1 (as qc[(l+3-1)%3]); qc[1] zeroed in RESET,
-//             qc[0] zeroed after the last round (or by the caller before the loop)
-//   wlc[r&1]  read in DISCHARGE of round r, appended in round r-1, zeroed in RIE r
-//   rlc[r&1]  appended in DISCHARGE r, read in RIE r; rlc[(r+1)&1] zeroed in RIE r
-// Requires qc[0][*] == 0 and wlc[*] == 0 on entry.
+//   qc/fs[l%3]  appended at level l-1 (RESET for l=0), read at level l, zeroed at
+//               level l+1; [1] zeroed in RESET; [0] zeroed in every RIE phase (or by
+//               the caller before the loop)
+//   wlc[r&1]    read in DISCHARGE of round r, appended in round r-1, zeroed in RIE r
+//   rlc[r&1]    appended in DISCHARGE r, read in RIE r; rlc[(r+1)&1] zeroed in RIE r
+//   bulc[l&1]   appended in pass A of level l, read in pass B; [(l+1)&1] zeroed at l
+//   mu          accumulated in RESET, read at level 0; zeroed with qc[0]
+// Requires qc[0], fs[0], mu == 0 and wlc == 0 on entry.
 __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseClock &clk, int kind,
                             const Lists &L, bool collect, bool stage2) {
   const int32_t n = d.n;
@@ -430,67 +786,122 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
   const int32_t nt = gridDim.x * NT;
   const uint8_t reg0 = kind == RK_PP ? PART_T : (kind == RK_STAGE2 ? PART_P : 0);
   const uint8_t reg1 = kind == RK_PP ? PART_S : 0;
+  const bool use0 = kind != RK_MINCUT, use1 = kind == RK_PP || kind == RK_MINCUT;
   const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
   for (int iter = 0;; ++iter) {
     // ---------------- RESET: heights of the domain, roots -> frontier level 0
-    if (blockIdx.x == 0 && threadIdx.x < 6) {
+    if (blockIdx.x == 0 && threadIdx.x < 2 * NB) {
       rlc[threadIdx.x] = 0;
-      if (threadIdx.x < 3) qc[3 + threadIdx.x] = 0;
-      if (threadIdx.x < 2) ctl->work[threadIdx.x] = 0;
+      if (threadIdx.x < NB) qc[NB + threadIdx.x] = 0;
+      if (threadIdx.x < 2) { ctl->work[threadIdx.x] = 0; ctl->fs[2 + threadIdx.x] = 0; ctl->bulc[threadIdx.x] = 0; }
     }
+    const int32_t N = kind == RK_STAGE2 ? ldv(&ctl->pcnt) : n;
+    const int32_t *dom = kind == RK_STAGE2 ? d.plist : nullptr;
     {
-      BL f0{L.q[0], qc, n};
-      const int32_t N = kind == RK_STAGE2 ? ldv(&ctl->pcnt) : n;
-      const int32_t wbase = blockIdx.x * NT + (threadIdx.x & ~31);
-      for (int32_t b = wbase; b < N; b += nt) {
-        const int32_t x = b + (threadIdx.x & 31);
-        bool r0 = false, r1 = false;
-        int32_t v = x;
-        if (x < N) {
-          if (kind == RK_STAGE2) v = d.plist[x];
+      long long fs0 = 0, fs1 = 0, mu0 = 0, mu1 = 0;
+      BL f0{L.q[0], qc, n, L.qc[0]};
+      compact_domain(d, sm.ts, N, dom, f0, BL{L.wl[0], wlc, n, nullptr}, false,
+        [&](int32_t v, int &tr, bool &front, bool &act) {
           const long long ev = ldv(d.e + v);
+          bool r0 = false, r1 = false, in0 = false, in1 = false;
           if (kind == RK_PUSH || kind == RK_MAXCUT) {
             r0 = v == d.t || (v != d.s && ev < 0);
+            in0 = v != d.s;
             d.hp[v] = r0 ? 0 : n;
           } else if (kind == RK_PP) {
             const uint8_t p = ldv(d.part + v);
-            r0 = p == PART_T && (v == d.t || (v != d.s && ev < 0));
-            r1 = p == PART_S && (v == d.s || (v != d.t && ev > 0));
+            in0 = p == PART_T && v != d.s;
+            in1 = p == PART_S && v != d.t;
+            r0 = in0 && (v == d.t || ev < 0);
+            r1 = in1 && (v == d.s || ev > 0);
             d.hp[v] = r0 ? 0 : n;
             d.hm[v] = r1 ? 0 : n;
           } else if (kind == RK_STAGE2) {
             r0 = ev < 0;
+            in0 = true;
             d.hp[v] = r0 ? 0 : n;
           } else {  // RK_MINCUT
             r1 = v == d.s || (v != d.t && ev > 0);
+            in1 = v != d.t;
             d.hm[v] = r1 ? 0 : n;
           }
-        }
-        bl_append_conv(d, f0, r0, v, 0u);
-        bl_append_conv(d, f0, r1, v, TRACK_BIT);
+          if ((in0 && !r0) || (in1 && !r1)) {
+            const long long deg = d.row[v + 1] - d.row[v];
+            if (in0 && !r0) mu0 += deg; else mu1 += deg;
+          }
+          front = r0 || r1;
+          tr = r1 ? 1 : 0;
+          act = false;
+        }, fs0, fs1);
+      BlockG bg{sm.red};
+      fs0 = bg.sum(fs0); fs1 = bg.sum(fs1); mu0 = bg.sum(mu0); mu1 = bg.sum(mu1);
+      if (threadIdx.x == 0) {
+        if (fs0) atomicAdd(ctl->fs, (unsigned long long)fs0);
+        if (fs1) atomicAdd(ctl->fs + 1, (unsigned long long)fs1);
+        if (mu0) atomicAdd(ctl->mu, (unsigned long long)mu0);
+        if (mu1) atomicAdd(ctl->mu + 1, (unsigned long long)mu1);
       }
       if (lead) sstat_add(sm, ST_RESET_V, (unsigned long long)N);
     }
     beacon(d, 10 + kind, iter, 0, 0);
     grid.sync();
-    clk.lap(sm, ST_T_RESET);
+    clk.lap(d, sm, ST_T_RESET, iter, kind, N);
     // ---------------- BFS levels (fused worklist compaction + termination test)
+    long long mu[2] = {use0 ? ldv(reinterpret_cast<const long long *>(ctl->mu)) : 0,
+                       use1 ? ldv(reinterpret_cast<const long long *>(ctl->mu + 1)) : 0};
     int32_t lvl = 0;
     for (;; ++lvl) {
-      int32_t *cur_c = qc + 3 * (lvl % 3);
-      const int32_t c[3] = {ldv(cur_c), ldv(cur_c + 1), ldv(cur_c + 2)};
-      beacon(d, 20 + kind, iter, 0, lvl, c[0] + c[1] + c[2], c[2]);
-      if (c[0] + c[1] + c[2] == 0) break;
-      if (blockIdx.x == 0 && threadIdx.x < 3) qc[3 * ((lvl + 2) % 3) + threadIdx.x] = 0;
-      BfsCtx ctx{lvl, reg0, reg1, collect, BL{L.q[(lvl + 1) & 1], qc + 3 * ((lvl + 1) % 3), n}, BL{L.wl[0], wlc, n}};
-      bfs_level(d, sm, BL{L.q[lvl & 1], cur_c, n}, c, ctx);
-      grid.sync();
-      clk.lap(sm, ST_T_BFS);
+      int32_t *cur_c = qc + NB * (lvl % 3);
+      int32_t c[NB];
+      read_counts(cur_c, c);
+      beacon(d, 20 + kind, iter, 0, lvl, total(c), c[3]);
+      if (total(c) == 0) break;
+      unsigned long long *fs = ctl->fs + 2 * (lvl % 3);
+      const long long f0 = ldv(reinterpret_cast<const long long *>(fs));
+      const long long f1 = ldv(reinterpret_cast<const long long *>(fs + 1));
+      if (lvl > 0) { mu[0] -= f0; mu[1] -= f1; }
+      if (blockIdx.x == 0 && threadIdx.x < NB) {
+        qc[NB * ((lvl + 2) % 3) + threadIdx.x] = 0;
+        if (threadIdx.x < 2) {
+          ctl->fs[2 * ((lvl + 2) % 3) + threadIdx.x] = 0;
+          ctl->bulc[2 * ((lvl + 1) & 1) + threadIdx.x] = 0;
+        }
+      }
+      const bool bu0 = f0 > 0 && (unsigned long long)f0 * BU_ALPHA > (unsigned long long)(mu[0] > 0 ? mu[0] : 0);
+      const bool bu1 = f1 > 0 && (unsigned long long)f1 * BU_ALPHA > (unsigned long long)(mu[1] > 0 ? mu[1] : 0);
+      const bool sparse = !bu0 && !bu1 && (unsigned long long)(f0 + f1) * SPARSE_DIV < (unsigned long long)d.S;
+      const BL nextl{L.q[(lvl + 1) & 1], qc + NB * ((lvl + 1) % 3), n, L.qc[(lvl + 1) & 1]};
+      const BL wll{L.wl[0], wlc, n, nullptr};
+      BfsCtx ctx{lvl, reg0, reg1, collect, {bu0, bu1}, sparse, nextl, wll, ctl->fs + 2 * ((lvl + 1) % 3)};
+      if (lead && (bu0 || bu1)) sstat_add(sm, ST_BU_LEVELS, 1);
+      bfs_expand_level(d, grid, sm, BL{L.q[lvl & 1], cur_c, n, L.qc[lvl & 1]}, c, ctx, d.bul,
+                       ctl->bulc + 2 * (lvl & 1));
+      if (!sparse) {                                // DENSE: build level lvl+1 by compaction
+        long long fs0 = 0, fs1 = 0;
+        compact_domain(d, sm.ts, N, dom, nextl, wll, collect,
+          [&](int32_t v, int &tr, bool &front, bool &act) {
+            if (use0 && ldv(d.hp + v) == lvl + 1) { tr = 0; front = true; }
+            else if (use1 && ldv(d.hm + v) == lvl + 1) { tr = 1; front = true; }
+            if (front && collect) {
+              const long long ev = ldv(d.e + v);
+              act = tr ? (ev < 0) : (ev > 0);
+            }
+          }, fs0, fs1);
+        BlockG bg{sm.red};
+        fs0 = bg.sum(fs0); fs1 = bg.sum(fs1);
+        if (threadIdx.x == 0) {
+          if (fs0) atomicAdd(ctx.fs_next, (unsigned long long)fs0);
+          if (fs1) atomicAdd(ctx.fs_next + 1, (unsigned long long)fs1);
+        }
+        grid.sync();
+      }
+      clk.lap(d, sm, ST_T_BFS, iter, lvl, total(c), (bu0 ? 1 : 0) | (bu1 ? 2 : 0) | (sparse ? 4 : 0) | (c[3] << 3));
     }
     if (lead) sstat_add(sm, ST_LEVELS, (unsigned long long)lvl);
     {
-      const int32_t w0 = ldv(wlc) + ldv(wlc + 1) + ldv(wlc + 2);
-      if (w0 == 0) break;                         // no active vertex: converged (R9)
+      int32_t w0[NB];
+      read_counts(wlc, w0);
+      if (total(w0) == 0) break;                  // no active vertex: converged (R9)
     }
     if (lead) {
       sstat_add(sm, ST_ITERS, 1);
@@ -504,41 +915,47 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
     unsigned long long spent = 0;                 // work since the global relabel (same in every thread)
     for (int r = 0;; ++r) {
       const int cur = r & 1, nx = cur ^ 1;
-      const int32_t w[3] = {ldv(wlc + 3 * cur), ldv(wlc + 3 * cur + 1), ldv(wlc + 3 * cur + 2)};
-      beacon(d, 30 + kind, iter, r, 0, w[0] + w[1] + w[2], w[2]);
-      BL nxt{L.wl[nx], wlc + 3 * nx, n};
-      BL rl{L.rl, rlc + 3 * cur, n};
-      process_bl(BL{L.wl[cur], wlc + 3 * cur, n}, w, sm,
+      int32_t w[NB];
+      read_counts(wlc + NB * cur, w);
+      beacon(d, 30 + kind, iter, r, 0, total(w), w[3]);
+      BL nxt{L.wl[nx], wlc + NB * nx, n, nullptr};
+      BL rl{L.rl, rlc + NB * cur, n, L.rlc};
+      process_bl(BL{L.wl[cur], wlc + NB * cur, n, nullptr}, w, sm,
                  [&](auto &g, int32_t entry) { discharge(d, g, sm, entry, rl, nxt, ctl->work + cur); });
       grid.sync();
-      clk.lap(sm, ST_T_DIS);
-      if (blockIdx.x == 0 && threadIdx.x < 3) {
-        wlc[3 * cur + threadIdx.x] = 0;
-        rlc[3 * nx + threadIdx.x] = 0;
+      clk.lap(d, sm, ST_T_DIS, iter, r, total(w), w[3]);
+      if (blockIdx.x == 0 && threadIdx.x < NB) {
+        wlc[NB * cur + threadIdx.x] = 0;
+        rlc[NB * nx + threadIdx.x] = 0;
         qc[threadIdx.x] = 0;                      // for the next RESET
+        if (threadIdx.x < 2) { ctl->fs[threadIdx.x] = 0; ctl->mu[threadIdx.x] = 0; }
         if (threadIdx.x == 0) ctl->work[nx] = 0;  // read at the end of round r-1
       }
+      int32_t rc[NB];
+      read_counts(rlc + NB * cur, rc);
       {
-        const int32_t rc[3] = {ldv(rlc + 3 * cur), ldv(rlc + 3 * cur + 1), ldv(rlc + 3 * cur + 2)};
-        beacon(d, 40 + kind, iter, r, 0, rc[0] + rc[1] + rc[2], rc[2]);
-        process_bl(rl, rc, sm, [&](auto &g, int32_t entry) { rie(d, g, sm, entry, nxt, ctl->work + cur); });
+        beacon(d, 40 + kind, iter, r, 0, total(rc), rc[3]);
+        rie_chunks(d, sm, rl.cq, rc[3], nxt, ctl->work + cur);
+        const int32_t rc2[NB] = {rc[0], rc[1], 0, 0};
+        process_bl(rl, rc2, sm, [&](auto &g, int32_t entry) { rie(d, g, sm, entry, nxt, ctl->work + cur); });
       }
       if (lead) sstat_add(sm, ST_ROUNDS, 1);
       grid.sync();
-      clk.lap(sm, ST_T_RIE);
-      const int32_t wn[3] = {ldv(wlc + 3 * nx), ldv(wlc + 3 * nx + 1), ldv(wlc + 3 * nx + 2)};
+      clk.lap(d, sm, ST_T_RIE, iter, r, total(rc), rc[3]);
+      int32_t wn[NB];
+      read_counts(wlc + NB * nx, wn);
       spent += (unsigned long long)ldv(reinterpret_cast<const long long *>(ctl->work + cur));
-      if (wn[0] + wn[1] + wn[2] == 0) break;
+      if (total(wn) == 0) break;
       if (r + 1 >= MAX_ROUNDS || (long long)spent > d.work_budget) {   // hand the rest to a global relabel
         if (lead) sstat_add(sm, ST_BUDGET_STOPS, 1);
-        for (int b = 0; b < 3; b++) {
+        for (int b = 0; b < NB; b++) {
           const int32_t *lst = nxt.bin(b);
           for (int32_t x = blockIdx.x * NT + threadIdx.x; x < wn[b]; x += nt)
             d.inq[(uint32_t)lst[x] & ~TRACK_BIT] = 0;
         }
         grid.sync();                              // everyone has read wn before this
-        clk.lap(sm, ST_T_DIS);
-        if (blockIdx.x == 0 && threadIdx.x < 3) wlc[3 * nx + threadIdx.x] = 0;
+        clk.lap(d, sm, ST_T_DIS, iter, -1);
+        if (blockIdx.x == 0 && threadIdx.x < NB) wlc[NB * nx + threadIdx.x] = 0;
         break;
       }
     }
@@ -582,15 +999,15 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(Dev d, int32_t m
   const int32_t n = d.n;
   const int32_t gt = blockIdx.x * NTHREADS + threadIdx.x, nt = gridDim.x * NTHREADS;
   Ctl *ctl = d.ctl;
-  const size_t n3 = 3 * (size_t)n;
-  const Lists L{{d.q0, d.q1}, {d.wl, d.wl + n3}, d.rl};
+  const size_t nb = (size_t)NB * n;
+  const Lists L{{d.q0, d.q1}, {d.cq0, d.cq1}, {d.wl, d.wl + nb}, d.rl, d.cqr};
   BlockG bg{sm.red};
   PhaseClock clk;
   clk.start();
 
   if (mode == MODE_STATIC) {
     // Alg.1 l.1-8: e = 0, c_f = c  (and the mirror)
-    for (int64_t i = gt; i < d.S; i += nt) { const int32_t c = d.cap[i]; d.res[i] = c; d.rres[d.rev[i]] = c; }
+    for (int64_t i = gt; i < d.S; i += nt) { d.res[i] = d.cap[i]; d.rres[i] = d.cap[d.rev[i]]; }
     for (int32_t v = gt; v < n; v += nt) d.e[v] = 0;
     grid.sync();
   } else if (mode == MODE_PR || mode == MODE_PP) {
@@ -648,7 +1065,7 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(Dev d, int32_t m
     tot = bg.sum(tot);
     if (threadIdx.x == 0 && tot) atom_add(d.e + d.s, -tot);
     grid.sync();
-    clk.lap(sm, ST_T_PRO);
+    clk.lap(d, sm, ST_T_PRO);
     device_loop(d, grid, sm, clk, RK_PUSH, L, true, false);
     // part from the final fresh BFS (S = unreached = S_max, R15) + flow (R8)
     long long f = 0;
@@ -661,10 +1078,13 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(Dev d, int32_t m
     if (threadIdx.x == 0 && f) atomicAdd(reinterpret_cast<unsigned long long *>(&ctl->flow), (unsigned long long)f);
   } else if (mode == MODE_PP) {
     // ---- stage 1: push on T || pull on S (Alg.8 l.15-28)
-    clk.lap(sm, ST_T_PRO);
+    clk.lap(d, sm, ST_T_PRO);
     device_loop(d, grid, sm, clk, RK_PP, L, true, false);
     // ---- P = {h+ = |V| and h- = |V|} (Alg.8 l.29-33), vertices with slots only
-    if (blockIdx.x == 0 && threadIdx.x < 3) ctl->qc[threadIdx.x] = 0;
+    if (blockIdx.x == 0 && threadIdx.x < NB) {
+      ctl->qc[threadIdx.x] = 0;
+      if (threadIdx.x < 2) { ctl->fs[threadIdx.x] = 0; ctl->mu[threadIdx.x] = 0; }
+    }
     for (int32_t b = blockIdx.x * NTHREADS + (threadIdx.x & ~31); b < n; b += nt) {
       const int32_t v = b + (threadIdx.x & 31);
       bool inP = false;
@@ -677,7 +1097,7 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(Dev d, int32_t m
     grid.sync();
     if (threadIdx.x == 0 && blockIdx.x == 0) sstat_add(sm, ST_S2_V, (unsigned long long)ldv(&ctl->pcnt));
     // ---- stage 2: Dynamic Push-Relabel restricted to P (Alg.8 l.34)
-    clk.lap(sm, ST_T_EPI);
+    clk.lap(d, sm, ST_T_EPI);
     if (ldv(&ctl->pcnt) > 0) device_loop(d, grid, sm, clk, RK_STAGE2, L, true, true);
     // ---- relabel partitions (Alg.8 l.35-49) and F (= sum over T' of e, R8)
     const int32_t pc = ldv(&ctl->pcnt);
@@ -697,7 +1117,7 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(Dev d, int32_t m
     for (int32_t v = gt; v < n; v += nt)
       d.mask[v] = mode == MODE_MINCUT ? (ldv(d.hm + v) < n ? 1 : 0) : (ldv(d.hp + v) < n ? 0 : 1);
   }
-  clk.lap(sm, ST_T_EPI);
+  clk.lap(d, sm, ST_T_EPI);
   __syncthreads();
   for (int i = threadIdx.x; i < ST_N; i += NTHREADS)
     if (sm.stat[i]) atomicAdd(&ctl->stat[i], sm.stat[i]);

@@ -8,7 +8,7 @@ import paper_2511_05895_b200 as P
 scale = int(sys.argv[1]) if len(sys.argv) > 1 else 12
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 keys = ("iterations", "rounds", "budget_stops", "bfs_levels", "bfs_slots", "discharge_vertices", "discharge_slots",
-        "pushes", "relabels", "activations", "stage2_vertices", "device_ms", "t_prologue_us", "t_reset_us", "t_bfs_us", "t_discharge_us", "t_rie_us", "t_epilogue_us")
+        "pushes", "relabels", "activations", "stage2_vertices", "bottom_up_levels", "device_ms", "t_prologue_us", "t_reset_us", "t_bfs_us", "t_discharge_us", "t_rie_us", "t_epilogue_us")
 g = W.rmat(scale, 16, 1, 7)
 f = P.DynMaxFlow.from_graph(g, max_iters=iters)
 F = f.static_solve()

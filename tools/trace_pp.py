@@ -1,0 +1,23 @@
+"""Print the per-phase trace of a PP batch / PR batch / static solve on RMAT-20."""
+import sys, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import workloads as W
+import paper_2511_05895_b200 as P
+
+scale = int(sys.argv[1]) if len(sys.argv) > 1 else 20
+g = W.rmat(scale, 16, 1, 7)
+f = P.DynMaxFlow.from_graph(g)
+f.set_trace(8192)
+def show(tag):
+    st = f.stats()
+    print(f"== {tag}: {st['device_ms']:.3f} ms")
+    for r in f.trace():
+        ex = r['extra']
+        extra = f"bu={ex & 3} sp={(ex >> 2) & 1} ch={ex >> 3}" if r['phase'] == 'bfs' else f"x={ex}"
+        print(f"  {r['phase']:9s} it={r['iter']:<3d} sub={r['sub']:<4d} items={r['items']:<9d} {extra:16s} {r['us']:9.1f} us")
+f.static_solve(); show("static")
+cs = W.CapState(g)
+for j, algo in enumerate(["pp", "pp", "pr"]):
+    b = W.rmat_batch(g, cs, 0.01, 100 + j); cs.apply(b)
+    f.apply_batch(b.u, b.v, b.new_cap, algo=algo); show(algo)
+m = f.min_cut_source_side(); show("mincut")
