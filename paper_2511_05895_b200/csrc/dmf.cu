@@ -66,7 +66,7 @@ struct dmf_graph {
   int32_t *plist = nullptr, *stamp = nullptr, *inq = nullptr, *bul = nullptr;
   long long *cq0 = nullptr, *cq1 = nullptr, *cqr = nullptr;
   long long *e = nullptr;
-  uint8_t *part = nullptr, *mask = nullptr;
+  uint8_t *part = nullptr, *mask = nullptr, *rlf = nullptr;
   int32_t *bbuf = nullptr;   // batch staging: u, v, c, slot  (4 * bcap)
   int64_t bcap = 0;
   Ctl *ctl = nullptr;
@@ -214,7 +214,7 @@ static Dev make_dev(dmf_graph *g) {
   d.row = g->row; d.dst = g->dst; d.rev = g->rev; d.cap = g->cap; d.res = g->res; d.rres = g->rres;
   d.e = g->e; d.hp = g->hp; d.hm = g->hm; d.part = g->part;
   d.q0 = g->q0; d.q1 = g->q1;
-  d.wl = g->wl; d.rl = g->rl; d.inq = g->inq; d.bul = g->bul;
+  d.wl = g->wl; d.rl = g->rl; d.inq = g->inq; d.bul = g->bul; d.rlf = g->rlf;
   d.cq0 = g->cq0; d.cq1 = g->cq1; d.cqr = g->cqr;
   d.plist = g->plist; d.stamp = g->stamp;
   d.mask = g->mask; d.ctl = g->ctl;
@@ -409,6 +409,7 @@ int dmf_create(int32_t n, const int64_t *row_ptr, const int32_t *col, const int3
   g->q1 = (int32_t *)g->alloc(NB * nn * 4);
   g->wl = (int32_t *)g->alloc(2 * NB * nn * 4);
   g->inq = (int32_t *)g->alloc(nn * 4);
+  g->rlf = (uint8_t *)g->alloc(nn);
   g->bul = (int32_t *)g->alloc(2 * nn * 4);
   const size_t cqn = (size_t)(S / CH) + nn + 64;   // >= sum over vertices of ceil(deg / CH)
   g->cq0 = (long long *)g->alloc(cqn * 8);
@@ -418,7 +419,7 @@ int dmf_create(int32_t n, const int64_t *row_ptr, const int32_t *col, const int3
   g->plist = (int32_t *)g->alloc(nn * 4);
   g->ctl = (Ctl *)g->alloc(sizeof(Ctl));
   if (!g->row || !g->dst || !g->rev || !g->cap || !g->res || !g->rres || !g->stamp || !g->e || !g->hp || !g->hm ||
-      !g->part || !g->mask || !g->q0 || !g->q1 || !g->wl || !g->rl || !g->plist || !g->ctl || !g->inq || !g->bul || !g->cq0 || !g->cq1 || !g->cqr) {
+      !g->part || !g->mask || !g->q0 || !g->q1 || !g->wl || !g->rl || !g->plist || !g->ctl || !g->inq || !g->rlf || !g->bul || !g->cq0 || !g->cq1 || !g->cqr) {
     fail(DMF_ENOMEM, "device allocation failed (state, S=%lld)", (long long)S);
     return bail(DMF_ENOMEM);
   }
@@ -430,6 +431,7 @@ int dmf_create(int32_t n, const int64_t *row_ptr, const int32_t *col, const int3
     CKB(cudaHostGetDevicePointer((void **)&g->ddbg, g->hdbg, 0));
   }
   CKB(cudaMemsetAsync(g->inq, 0, nn * 4, st));
+  CKB(cudaMemsetAsync(g->rlf, 0, nn, st));
   if (S) {
     CKB(cudaMemsetAsync(err, 0, 64, st));
     k_rows<<<blocks(nn + 1), TB, 0, st>>>(n, S, ukey, g->row);

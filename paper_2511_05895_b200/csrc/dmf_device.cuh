@@ -47,8 +47,8 @@ enum Stat : int {
 // Control block in device memory (zeroed by the host before every launch).
 struct Ctl {
   int32_t qc[3 * NB];   // BFS frontier counts [level % 3][degree bin]
-  int32_t wlc[2 * NB];  // active worklist counts [round & 1][degree bin]
-  int32_t rlc[2 * NB];  // relabelled-vertex list counts [round & 1][degree bin]
+  int32_t wlc[3 * NB];  // active worklist counts [round % 3][degree bin]
+  int32_t rlc[NB];      // relabelled-vertex list counts [degree bin] (one list per iteration)
   int32_t pcnt;         // |P| (push-pull stage 2 region)
   int32_t ntrace;       // trace records written
   int32_t status;       // dmf_status of the call (0 = OK)
@@ -56,7 +56,7 @@ struct Ctl {
   int32_t iters;
   int32_t pad;
   long long flow;       // F
-  unsigned long long work[2];   // discharge + RIE work of the current / previous round
+  unsigned long long work[3];   // discharge work per round [round % 3]
   unsigned long long fs[6];     // frontier slot counts [level % 3][track] (direction-optimising BFS)
   int32_t bulc[4];              // bottom-up candidate queue counts [level & 1][warp/CTA bin]
   unsigned long long mu[2];     // slots of the still-unlabelled vertices per track (BFS direction choice)
@@ -87,6 +87,7 @@ struct Dev {
   int32_t *wl;               // active worklists [2 rounds][NB bins][n]
   int32_t *rl;               // relabelled vertices [NB bins][n] (RemoveInvalidEdges scope, R13)
   int32_t *inq;              // per-vertex "queued for the next discharge round" flag
+  uint8_t *rlf;              // per-vertex "already in the relabelled list" flag
   int32_t *bul;              // bottom-up candidate queue [2 bins][n]
   long long *cq0, *cq1, *cqr; // chunk queues of the frontier ping-pong and of the relabelled list
   int32_t *plist;            // region P of push-pull stage 2

@@ -46,6 +46,7 @@ struct Smem {
   long long red[WPB + 1];
   unsigned long long stat[ST_N];
   TileSm ts;
+  long long budget[WPB + 1];   // push budgets: one per warp group + one for the CTA group
 };
 
 // Phase clock (block 0, thread 0): time between consecutive grid barriers is
@@ -567,11 +568,14 @@ __device__ __forceinline__ void bfs_expand_level(const Dev &d, cg::grid_group &g
 
 // ---------------------------------------------------------------------------
 // Discharge of one active vertex (Alg.2 / Alg.6): up to KERNELCYCLES cycles of
-// "scan residual out-slots for the lowest neighbour (h, slot); push if h(u) > h^,
-// else lift h(u) = h^+1" (clamped to n, R4/R5; ties by slot index, R6).  A push
-// cycle pushes to the successive lowest neighbours at height h^ in slot order until
-// the excess is gone -- exactly the run of Alg.2 cycles that would follow with the
-// heights as read.
+// "find the lowest residual neighbour (h^, slot); push if h(u) > h^, else lift
+// h(u) = h^+1" (clamped to n, R4/R5; ties by slot index, R6).
+//  * A push cycle pushes to the successive lowest neighbours at height h^ in slot
+//    order until the excess is gone -- exactly the run of Alg.2 cycles that would
+//    follow with the heights as read.
+//  * The same pass records the lowest height among slots that stay residual, so if
+//    excess remains (every admissible slot saturated) the lift goes straight to that
+//    minimum + 1 and the next cycle pushes without a separate argmin scan.
 template <class G>
 __device__ __forceinline__ void discharge(const Dev &d, const G &g, Smem &sm, int32_t entry, const BL &rl,
                                           const BL &nxt, unsigned long long *workc) {
@@ -583,6 +587,7 @@ __device__ __forceinline__ void discharge(const Dev &d, const G &g, Smem &sm, in
   const int32_t beg = d.row[u], end = d.row[u + 1];
   if (g.rank() == 0) { d.inq[u] = 0; __threadfence(); }
   int32_t hu = ldv(k.hgt + u);
+  int32_t hhat = -1;                   // current lowest residual-neighbour height (-1: unknown)
   bool relabelled = false;
   unsigned long long scanned = 0, pushes = 0, lifts = 0;
   long long eu = 0;
@@ -591,79 +596,115 @@ __device__ __forceinline__ void discharge(const Dev &d, const G &g, Smem &sm, in
     if (g.rank() == 0) eu = ldv(d.e + u) * k.sign;
     eu = g.bcast(eu);
     if (hu >= n || eu <= 0) break;
-    unsigned long long best = ~0ull;
-    for (int32_t i0 = beg + g.rank(); i0 < end; i0 += 4 * G::size) {
-      int32_t r[4], v[4];
+    if (hhat < 0) {                      // argmin scan (Alg.2 l.6-14)
+      unsigned long long best = ~0ull;
+      for (int32_t i0 = beg + g.rank(); i0 < end; i0 += 4 * G::size) {
+        int32_t r[4], v[4];
 #pragma unroll
-      for (int j = 0; j < 4; j++) {             // independent loads first (ILP), then the gathers
+        for (int j = 0; j < 4; j++) {   // independent loads first (ILP), then the gathers
+          const int32_t i = i0 + j * G::size;
+          r[j] = i < end ? ldv(k.F + i) : 0;
+          v[j] = i < end ? d.dst[i] : 0;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+          if (r[j] > 0) {
+            const int32_t h = ldv(k.hgt + v[j]);
+            best = (unsigned long long)(uint32_t)h < best ? (unsigned long long)(uint32_t)h : best;
+          }
+        }
+      }
+      scanned += (unsigned long long)(end - beg);
+      best = g.min(best);
+      if (best == ~0ull) {               // no residual out-edge: h^ = inf -> |V| (R4)
+        hu = n;
+        if (g.rank() == 0) k.hgt[u] = n;
+        relabelled = true;
+        lifts++;
+        break;
+      }
+      hhat = (int32_t)best;
+    }
+    if (hu <= hhat) {                    // lift(u) (Alg.2 l.21), clamped to |V| (R5)
+      hu = hhat + 1 < n ? hhat + 1 : n;
+      if (g.rank() == 0) k.hgt[u] = hu;
+      relabelled = true;
+      lifts++;
+      continue;
+    }
+    // push(u, v^) at height h^ (Alg.2 l.15-19), batched: the excess is a budget the
+    // lanes claim with shared-memory atomics (pushes to equal-height neighbours in
+    // any order; R6's slot order only fixes a tie-break that F and S_min ignore)
+    long long remaining = eu;
+    unsigned long long nmin = ~0ull;     // lowest height among slots left residual
+    long long *bud = G::size == 1 ? nullptr : (G::size == NT ? &sm.budget[WPB] : &sm.budget[threadIdx.x >> 5]);
+    if (G::size > 1) {
+      if (g.rank() == 0) *bud = eu;
+      if (G::size == NT) __syncthreads(); else __syncwarp();
+    }
+    for (int32_t i0 = beg + g.rank(); i0 < end; i0 += 4 * G::size) {
+      if (G::size == 1 ? remaining <= 0 : *((volatile long long *)bud) <= 0) break;
+      int32_t r[4], v[4], h[4];
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
         const int32_t i = i0 + j * G::size;
         r[j] = i < end ? ldv(k.F + i) : 0;
         v[j] = i < end ? d.dst[i] : 0;
       }
 #pragma unroll
+      for (int j = 0; j < 4; j++) h[j] = r[j] > 0 ? ldv(k.hgt + v[j]) : 0;
+#pragma unroll
       for (int j = 0; j < 4; j++) {
-        if (r[j] > 0) {
-          const int32_t h = ldv(k.hgt + v[j]);
-          const unsigned long long key = ((unsigned long long)(uint32_t)h << 32) | (uint32_t)(i0 + j * G::size - beg);
-          best = key < best ? key : best;
+        if (r[j] <= 0) continue;
+        long long take = 0;
+        if (h[j] == hhat) {
+          long long old;
+          if (G::size == 1) { old = remaining; remaining -= r[j]; }
+          else old = (long long)atomicAdd(reinterpret_cast<unsigned long long *>(bud),
+                                          (unsigned long long)(-(long long)r[j]));
+          take = old < 0 ? 0 : (old < r[j] ? old : r[j]);
         }
-      }
-    }
-    scanned += (unsigned long long)(end - beg);
-    best = g.min(best);
-    if (best == ~0ull) {                 // no residual out-edge: h^ = inf -> |V| (R4)
-      hu = n;
-      if (g.rank() == 0) k.hgt[u] = n;
-      relabelled = true;
-      lifts++;
-      break;
-    }
-    const int32_t hhat = (int32_t)(best >> 32);
-    if (hu > hhat) {                     // push(u, v^) applicable (Alg.2 l.15-19)
-      long long remaining = eu;
-      const int32_t start = beg + (int32_t)(best & 0xffffffffu);
-      for (int32_t base = start; base < end && remaining > 0; base += G::size) {
-        const int32_t i = base + g.rank();
-        long long amt = 0;
-        int32_t v = -1;
-        if (i < end) {
-          const int32_t r = ldv(k.F + i);
-          if (r > 0) {
-            v = d.dst[i];
-            if (ldv(k.hgt + v) == hhat) amt = r;
-          }
-        }
-        long long tot;
-        const long long ex = g.exscan(amt, tot);
-        long long take = remaining - ex;
-        take = take < 0 ? 0 : (take > amt ? amt : take);
         if (take > 0) {
+          const int32_t i = i0 + j * G::size;
           const int32_t ri = d.rev[i];
           atomicSub(k.F + i, (int32_t)take);       // c_f(u,v^) -= d
           atomicSub(k.R + ri, (int32_t)take);      //   mirror
           atomicAdd(k.F + ri, (int32_t)take);      // c_f(v^,u) += d
           atomicAdd(k.R + i, (int32_t)take);       //   mirror
-          const long long old = (long long)atomicAdd(reinterpret_cast<unsigned long long *>(d.e + v),
-                                                     (unsigned long long)(take * k.sign));   // e(v^) += d
-          const long long eo = old * k.sign;
-          if (eo <= 0 && eo + take > 0) activate(d, k, nxt, v, tag, sm);
+          const long long oe = (long long)atomicAdd(reinterpret_cast<unsigned long long *>(d.e + v[j]),
+                                                    (unsigned long long)(take * k.sign));   // e(v^) += d
+          const long long eo = oe * k.sign;
+          if (eo <= 0 && eo + take > 0) activate(d, k, nxt, v[j], tag, sm);
           pushes++;
         }
-        remaining -= tot;
-        scanned += (unsigned long long)G::size;
+        if (take < r[j]) nmin = (unsigned long long)(uint32_t)h[j] < nmin ? (unsigned long long)(uint32_t)h[j] : nmin;
       }
-      const long long done = eu - (remaining > 0 ? remaining : 0);
-      if (g.rank() == 0 && done > 0) atom_add(d.e + u, -done * k.sign);   // e(u) -= d
-    } else {                             // lift(u) (Alg.2 l.21), clamped to |V| (R5)
-      hu = hhat + 1 < n ? hhat + 1 : n;
-      if (g.rank() == 0) k.hgt[u] = hu;
-      relabelled = true;
-      lifts++;
+    }
+    scanned += (unsigned long long)(end - beg);
+    if (G::size > 1) {
+      if (G::size == NT) __syncthreads(); else __syncwarp();
+      remaining = *bud;
+      if (G::size == NT) __syncthreads(); else __syncwarp();
+    }
+    const long long done = eu - (remaining > 0 ? remaining : 0);
+    if (g.rank() == 0 && done > 0) atom_add(d.e + u, -done * k.sign);   // e(u) -= d
+    if (remaining > 0) {                 // every admissible slot saturated
+      nmin = g.min(nmin);
+      if (nmin == ~0ull) {               // nothing residual any more: lift to |V|
+        hu = n;
+        if (g.rank() == 0) k.hgt[u] = n;
+        relabelled = true;
+        lifts++;
+        break;
+      }
+      hhat = (int32_t)nmin;              // next cycle lifts (if h(u) <= h^) or pushes at h^
+    } else {
+      hhat = -1;                         // excess gone; rescan if more arrives
     }
   }
   if (g.rank() == 0) {
     if (cyc == d.kc && hu < n && ldv(d.e + u) * k.sign > 0) activate(d, k, nxt, u, tag, sm);  // KC spent
-    if (relabelled) bl_append_one(d, rl, u, tag);
+    if (relabelled && d.rlf[u] == 0) { d.rlf[u] = 1; bl_append_one(d, rl, u, tag); }
     atomicAdd(workc, scanned + 16ull * lifts + 16ull);
     sstat_add(sm, ST_DIS_V, 1);
     sstat_add(sm, ST_DIS_SLOTS, scanned);
@@ -695,7 +736,7 @@ __device__ __forceinline__ void rie_slots(const Dev &d, const Track &k, int32_t 
         const long long old = (long long)atomicAdd(reinterpret_cast<unsigned long long *>(d.e + v),
                                                    (unsigned long long)((long long)r * k.sign));
         const long long eo = old * k.sign;
-        if (eo <= 0 && eo + r > 0) activate(d, k, nxt, v, tag, sm);
+        (void)eo; (void)nxt;             // the next global relabel finds newly active vertices
         moved += r;
         sat++;
       }
@@ -712,6 +753,7 @@ __device__ __forceinline__ void rie(const Dev &d, const G &g, Smem &sm, int32_t 
   const Track k = make_track(d, tr);
   const int32_t beg = d.row[u], end = d.row[u + 1];
   const int32_t hu = ldv(k.hgt + u);
+  if (g.rank() == 0) d.rlf[u] = 0;
   long long moved = 0;
   unsigned long long sat = 0;
   rie_slots(d, k, u, hu, beg + g.rank(), end, G::size, tag, nxt, sm, moved, sat);
@@ -740,6 +782,7 @@ __device__ __forceinline__ void rie_chunks(const Dev &d, Smem &sm, const long lo
     const int32_t beg = d.row[u] + (int32_t)(ce >> 32) * CH;
     const int32_t end = min(d.row[u + 1], beg + CH);
     const int32_t hu = ldv(k.hgt + u);
+    if (lane == 0) d.rlf[u] = 0;
     long long moved = 0;
     unsigned long long sat = 0;
     rie_slots(d, k, u, hu, beg + lane, end, 32, tag, nxt, sm, moved, sat);
@@ -773,8 +816,10 @@ struct Lists {
 //   qc/fs[l%3]  appended at level l-1 (RESET for l=0), read at level l, zeroed at
 //               level l+1; [1] zeroed in RESET; [0] zeroed in every RIE phase (or by
 //               the caller before the loop)
-//   wlc[r&1]    read in DISCHARGE of round r, appended in round r-1, zeroed in RIE r
-//   rlc[r&1]    appended in DISCHARGE r, read in RIE r; rlc[(r+1)&1] zeroed in RIE r
+//   wlc[r%3]    read in DISCHARGE of round r, appended in round r-1 (the BFS for r=0),
+//               zeroed in round r+1 (as wlc[(r+3-1)%3]) and all of them in the RIE phase
+//   rlc         appended in every DISCHARGE round of an iteration (once per vertex,
+//               rlf flag), read in the iteration's RIE phase, zeroed in RESET
 //   bulc[l&1]   appended in pass A of level l, read in pass B; [(l+1)&1] zeroed at l
 //   mu          accumulated in RESET, read at level 0; zeroed with qc[0]
 // Requires qc[0], fs[0], mu == 0 and wlc == 0 on entry.
@@ -790,10 +835,11 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
   const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
   for (int iter = 0;; ++iter) {
     // ---------------- RESET: heights of the domain, roots -> frontier level 0
-    if (blockIdx.x == 0 && threadIdx.x < 2 * NB) {
+    if (blockIdx.x == 0 && threadIdx.x < NB) {
       rlc[threadIdx.x] = 0;
-      if (threadIdx.x < NB) qc[NB + threadIdx.x] = 0;
-      if (threadIdx.x < 2) { ctl->work[threadIdx.x] = 0; ctl->fs[2 + threadIdx.x] = 0; ctl->bulc[threadIdx.x] = 0; }
+      qc[NB + threadIdx.x] = 0;
+      if (threadIdx.x < 3) ctl->work[threadIdx.x] = 0;
+      if (threadIdx.x < 2) { ctl->fs[2 + threadIdx.x] = 0; ctl->bulc[threadIdx.x] = 0; }
     }
     const int32_t N = kind == RK_STAGE2 ? ldv(&ctl->pcnt) : n;
     const int32_t *dom = kind == RK_STAGE2 ? d.plist : nullptr;
@@ -911,40 +957,34 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
       if (lead) ctl->status = -8;                // DMF_ENOCONV
       break;
     }
-    // ---------------- rounds of DISCHARGE (push || pull tracks) + RIE
+    // ---------------- rounds of DISCHARGE (push || pull tracks), then RIE once
+    // (Alg.1 l.168-169: PushRelabel, then RemoveInvalidEdges, then the next BFS)
     unsigned long long spent = 0;                 // work since the global relabel (same in every thread)
+    const BL rl{L.rl, rlc, n, L.rlc};
     for (int r = 0;; ++r) {
-      const int cur = r & 1, nx = cur ^ 1;
+      // wlc / work rings of 3: round r reads [r%3], fills [(r+1)%3]; a slot is zeroed
+      // only when every block has passed the barrier after its last read
+      const int cur = r % 3, nx = (r + 1) % 3, nn = (r + 2) % 3;
       int32_t w[NB];
       read_counts(wlc + NB * cur, w);
       beacon(d, 30 + kind, iter, r, 0, total(w), w[3]);
-      BL nxt{L.wl[nx], wlc + NB * nx, n, nullptr};
-      BL rl{L.rl, rlc + NB * cur, n, L.rlc};
-      process_bl(BL{L.wl[cur], wlc + NB * cur, n, nullptr}, w, sm,
-                 [&](auto &g, int32_t entry) { discharge(d, g, sm, entry, rl, nxt, ctl->work + cur); });
-      grid.sync();
-      clk.lap(d, sm, ST_T_DIS, iter, r, total(w), w[3]);
       if (blockIdx.x == 0 && threadIdx.x < NB) {
-        wlc[NB * cur + threadIdx.x] = 0;
-        rlc[NB * nx + threadIdx.x] = 0;
-        qc[threadIdx.x] = 0;                      // for the next RESET
-        if (threadIdx.x < 2) { ctl->fs[threadIdx.x] = 0; ctl->mu[threadIdx.x] = 0; }
-        if (threadIdx.x == 0) ctl->work[nx] = 0;  // read at the end of round r-1
+        wlc[NB * nn + threadIdx.x] = 0;           // last read in round r-1 (before its barrier)
+        if (threadIdx.x == 0) ctl->work[nx] = 0;  // last read at the end of round r-2; filled in round r+1
       }
-      int32_t rc[NB];
-      read_counts(rlc + NB * cur, rc);
-      {
-        beacon(d, 40 + kind, iter, r, 0, total(rc), rc[3]);
-        rie_chunks(d, sm, rl.cq, rc[3], nxt, ctl->work + cur);
-        const int32_t rc2[NB] = {rc[0], rc[1], 0, 0};
-        process_bl(rl, rc2, sm, [&](auto &g, int32_t entry) { rie(d, g, sm, entry, nxt, ctl->work + cur); });
-      }
+      const BL nxt{L.wl[(r + 1) & 1], wlc + NB * nx, n, nullptr};
+      process_bl(BL{L.wl[r & 1], wlc + NB * cur, n, nullptr}, w, sm,
+                 [&](auto &g, int32_t entry) { discharge(d, g, sm, entry, rl, nxt, ctl->work + cur); });
       if (lead) sstat_add(sm, ST_ROUNDS, 1);
       grid.sync();
-      clk.lap(d, sm, ST_T_RIE, iter, r, total(rc), rc[3]);
+      clk.lap(d, sm, ST_T_DIS, iter, r, total(w), w[3]);
       int32_t wn[NB];
       read_counts(wlc + NB * nx, wn);
-      spent += (unsigned long long)ldv(reinterpret_cast<const long long *>(ctl->work + cur));
+      // a round's barrier + latency floor is charged like S/16 scanned slots, so that
+      // long tails of near-empty rounds (excess creeping up one lift at a time) hand
+      // over to a global relabel, which lifts unreachable vertices to |V| at once
+      spent += (unsigned long long)ldv(reinterpret_cast<const long long *>(ctl->work + cur)) +
+               (unsigned long long)(d.S >> 4);
       if (total(wn) == 0) break;
       if (r + 1 >= MAX_ROUNDS || (long long)spent > d.work_budget) {   // hand the rest to a global relabel
         if (lead) sstat_add(sm, ST_BUDGET_STOPS, 1);
@@ -953,11 +993,24 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
           for (int32_t x = blockIdx.x * NT + threadIdx.x; x < wn[b]; x += nt)
             d.inq[(uint32_t)lst[x] & ~TRACK_BIT] = 0;
         }
-        grid.sync();                              // everyone has read wn before this
-        clk.lap(d, sm, ST_T_DIS, iter, -1);
-        if (blockIdx.x == 0 && threadIdx.x < NB) wlc[NB * nx + threadIdx.x] = 0;
-        break;
+        break;                                    // (the RIE barrier below publishes the flags)
       }
+    }
+    // ---------------- RIE over the vertices relabelled in this iteration
+    if (blockIdx.x == 0 && threadIdx.x < NB) {
+      for (int q = 0; q < 3; q++) wlc[NB * q + threadIdx.x] = 0;
+      qc[threadIdx.x] = 0;                        // for the next RESET
+      if (threadIdx.x < 2) { ctl->fs[threadIdx.x] = 0; ctl->mu[threadIdx.x] = 0; }
+    }
+    {
+      int32_t rc[NB];
+      read_counts(rlc, rc);
+      beacon(d, 40 + kind, iter, 0, 0, total(rc), rc[3]);
+      rie_chunks(d, sm, rl.cq, rc[3], rl, ctl->work);
+      const int32_t rc2[NB] = {rc[0], rc[1], 0, 0};
+      process_bl(rl, rc2, sm, [&](auto &g, int32_t entry) { rie(d, g, sm, entry, rl, ctl->work); });
+      grid.sync();
+      clk.lap(d, sm, ST_T_RIE, iter, 0, total(rc), rc[3]);
     }
   }
 }
