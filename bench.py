@@ -202,6 +202,7 @@ def main():
     import torch
     import torch.distributed as dist
     import paper_2511_05895_b200 as P
+    from paper_2511_05895_b200.replicas import reduce_job
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -251,6 +252,7 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = f.stats()["kernel_launches"]
     e0.record(stream)
     kernel_ms, alg_bytes, per = [], [], []
     k_tot = 0
@@ -265,6 +267,7 @@ def main():
     if world > 1:
         dist.barrier()
     elapsed_ms = e0.elapsed_time(e1)
+    launches = f.stats()["kernel_launches"] - launches0
 
     # ---- timed: end to end from pinned host buffers, F + mask back to the host
     if world > 1:
@@ -294,13 +297,7 @@ def main():
         assert np.array_equal(f.min_cut_source_side(), mask_dyn)
 
     # ---- reduce over ranks (one NCCL all_reduce each, outside the timed loops)
-    tot = torch.tensor([float(k_tot), float(k_e2e)], device=dev, dtype=torch.float64)
-    mx = torch.tensor([elapsed_ms, e2e_ms], device=dev, dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-    k_all, k_e2e_all = tot.tolist()
-    el_max, e2e_max = mx.tolist()
+    k_all, el_max, k_e2e_all, e2e_max = reduce_job(k_tot, elapsed_ms, k_e2e, e2e_ms, device=dev)
 
     if rank == 0:
         peak, peak_src = peaks()
@@ -332,7 +329,7 @@ def main():
             "e2e": {"value": k_e2e_all / (e2e_max * 1e-3), "unit": UNIT,
                     "h2d_bytes_per_step": int(3 * 4 * batches[0].k),
                     "d2h_bytes_per_step": int(8 + (0 if args.no_cut else g.n))},
-            "gpu_launches": int(K * (1 if args.no_cut else 2)),
+            "gpu_launches": int(launches),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": f"k_solve (mode {args.algo.upper()} batch launch)",
@@ -345,6 +342,8 @@ def main():
             "edges_per_s": g.m / (apply_ms * 1e-3),
             "static_edges_per_s": g.m / (static_med * 1e-3),
             "flow": {"F_static_initial": F_static0, "F_final": F_dyn},
+            "phase_us_median": {k: med(k) for k in ("t_prologue_us", "t_reset_us", "t_bfs_us", "t_discharge_us",
+                                                     "t_rie_us", "t_epilogue_us")},
             "per_batch_median": {k: med(k) for k in ("iterations", "rounds", "bfs_levels", "bfs_slots",
                                                      "discharge_vertices", "activations", "pushes", "relabels",
                                                      "stage2_vertices")},

@@ -93,6 +93,7 @@ typedef struct {
     int64_t reset_vertices;    /* vertices whose heights were reset for a global relabel */
     int64_t budget_stops;      /* discharge round sequences cut short by the work budget (-> global relabel) */
     int64_t bottom_up_levels;  /* BFS levels expanded bottom-up (direction-optimising BFS) */
+    int64_t kernel_launches;   /* CUMULATIVE kernels launched by solve/apply/cut calls since dmf_create */
     float   device_ms;         /* device time of the last call's kernel(s), CUDA events */
     /* in-kernel phase clock (%globaltimer, block 0), microseconds, last call:
      * prologue = batch validate/apply/clamp + source / S->T saturation,

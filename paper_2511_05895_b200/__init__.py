@@ -46,6 +46,7 @@ class Stats(ctypes.Structure):
                 ("batch_entries", ctypes.c_int64), ("stage2_vertices", ctypes.c_int64),
                 ("stage2_iterations", ctypes.c_int64), ("rounds", ctypes.c_int64), ("activations", ctypes.c_int64),
                 ("reset_vertices", ctypes.c_int64), ("budget_stops", ctypes.c_int64), ("bottom_up_levels", ctypes.c_int64),
+                ("kernel_launches", ctypes.c_int64),
                 ("device_ms", ctypes.c_float), ("t_prologue_us", ctypes.c_float), ("t_reset_us", ctypes.c_float),
                 ("t_bfs_us", ctypes.c_float), ("t_discharge_us", ctypes.c_float), ("t_rie_us", ctypes.c_float),
                 ("t_epilogue_us", ctypes.c_float)]

@@ -79,6 +79,8 @@ struct dmf_graph {
   double watchdog_s = 0;
   int32_t batch_id = 0;
   bool solved = false;
+  bool smin_valid = false;   // g->mask holds S_min of the current state
+  int64_t launches = 0;      // kernels launched by solve / apply / cut calls since create
   int64_t flow = 0;
   dmf_stats stats{};
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -226,11 +228,13 @@ static Dev make_dev(dmf_graph *g) {
 
 static int run_solve(dmf_graph *g, int32_t mode, const Dev &dv) {
   Dev d = dv;
+  if (mode != MODE_MINCUT) g->smin_valid = false;  // the state (or the mask buffer) is about to change
   CK(cudaMemsetAsync(g->ctl, 0, sizeof(Ctl), g->stream));
   CK(cudaEventRecord(g->ev0, g->stream));
   int32_t md = mode;
   void *args[] = {&d, &md};
   CK(cudaLaunchCooperativeKernel((const void *)k_solve<NT>, dim3(g->grid_blocks), dim3(NT), args, 0, g->stream));
+  g->launches++;
   CK(cudaEventRecord(g->ev1, g->stream));
   CK(cudaMemcpyAsync(g->hctl, g->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, g->stream));
   if (g->watchdog_s > 0) {             // debug watchdog: poll instead of blocking
@@ -291,6 +295,7 @@ static int run_solve(dmf_graph *g, int32_t mode, const Dev &dv) {
     g->flow = c.flow;
     g->solved = true;
   }
+  g->smin_valid = mode == MODE_PP || mode == MODE_MINCUT;   // MAXCUT / STATIC / PR leave no S_min
   return DMF_OK;
 }
 
@@ -530,11 +535,13 @@ static int cut_query(dmf_graph *g, uint8_t *mask, int32_t mode) {
   g_last_error.clear();
   if (!g || !mask) return fail(DMF_EINVAL, "NULL argument");
   if (!g->solved) return fail(DMF_ESTATE, "no converged solve yet");
-  dmf_stats keep = g->stats;
-  Dev d = make_dev(g);
-  int rc = run_solve(g, mode, d);
-  g->stats = keep;
-  if (rc) return rc;
+  if (!(mode == MODE_MINCUT && g->smin_valid)) {   // a DYN_PP repair already produced S_min
+    dmf_stats keep = g->stats;
+    Dev d = make_dev(g);
+    int rc = run_solve(g, mode, d);
+    g->stats = keep;
+    if (rc) return rc;
+  }
   CK(cudaMemcpyAsync(mask, g->mask, (size_t)g->n, cudaMemcpyDefault, g->stream));
   CK(cudaStreamSynchronize(g->stream));
   return DMF_OK;
@@ -570,6 +577,7 @@ int dmf_get_trace(const dmf_graph *g, int32_t *records, int32_t capacity, int32_
 int dmf_get_stats(const dmf_graph *g, dmf_stats *out) {
   if (!g || !out) return fail(DMF_EINVAL, "NULL argument");
   *out = g->stats;
+  out->kernel_launches = g->launches;
   return DMF_OK;
 }
 

@@ -798,7 +798,7 @@ __device__ __forceinline__ void rie_chunks(const Dev &d, Smem &sm, const long lo
 
 // ---------------------------------------------------------------------------
 // Roots of a global relabel.
-enum ResetKind : int { RK_PUSH = 0, RK_PP = 1, RK_STAGE2 = 2, RK_MINCUT = 3, RK_MAXCUT = 4 };
+enum ResetKind : int { RK_PUSH = 0, RK_PP = 1, RK_STAGE2 = 2, RK_MINCUT = 3, RK_MAXCUT = 4, RK_MINCUT_P = 5 };
 
 struct Lists {
   int32_t *q[2];    // frontier ping-pong, [NB bins][n] each
@@ -830,8 +830,10 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
   int32_t *qc = ctl->qc, *wlc = ctl->wlc, *rlc = ctl->rlc;
   const int32_t nt = gridDim.x * NT;
   const uint8_t reg0 = kind == RK_PP ? PART_T : (kind == RK_STAGE2 ? PART_P : 0);
-  const uint8_t reg1 = kind == RK_PP ? PART_S : 0;
-  const bool use0 = kind != RK_MINCUT, use1 = kind == RK_PP || kind == RK_MINCUT;
+  const uint8_t reg1 = kind == RK_PP ? PART_S : (kind == RK_MINCUT_P ? PART_P : 0);
+  const bool use0 = kind != RK_MINCUT && kind != RK_MINCUT_P;
+  const bool use1 = kind == RK_PP || kind == RK_MINCUT || kind == RK_MINCUT_P;
+  const bool on_plist = kind == RK_STAGE2 || kind == RK_MINCUT_P;
   const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
   for (int iter = 0;; ++iter) {
     // ---------------- RESET: heights of the domain, roots -> frontier level 0
@@ -841,8 +843,8 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
       if (threadIdx.x < 3) ctl->work[threadIdx.x] = 0;
       if (threadIdx.x < 2) { ctl->fs[2 + threadIdx.x] = 0; ctl->bulc[threadIdx.x] = 0; }
     }
-    const int32_t N = kind == RK_STAGE2 ? ldv(&ctl->pcnt) : n;
-    const int32_t *dom = kind == RK_STAGE2 ? d.plist : nullptr;
+    const int32_t N = on_plist ? ldv(&ctl->pcnt) : n;
+    const int32_t *dom = on_plist ? d.plist : nullptr;
     {
       long long fs0 = 0, fs1 = 0, mu0 = 0, mu1 = 0;
       BL f0{L.q[0], qc, n, L.qc[0]};
@@ -866,6 +868,10 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
             r0 = ev < 0;
             in0 = true;
             d.hp[v] = r0 ? 0 : n;
+          } else if (kind == RK_MINCUT_P) {     // forward reach of the excess left in P
+            r1 = ev > 0;
+            in1 = true;
+            d.hm[v] = r1 ? 0 : n;
           } else {  // RK_MINCUT
             r1 = v == d.s || (v != d.t && ev > 0);
             in1 = v != d.t;
@@ -1151,9 +1157,20 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(Dev d, int32_t m
     if (threadIdx.x == 0 && blockIdx.x == 0) sstat_add(sm, ST_S2_V, (unsigned long long)ldv(&ctl->pcnt));
     // ---- stage 2: Dynamic Push-Relabel restricted to P (Alg.8 l.34)
     clk.lap(d, sm, ST_T_EPI);
-    if (ldv(&ctl->pcnt) > 0) device_loop(d, grid, sm, clk, RK_STAGE2, L, true, true);
-    // ---- relabel partitions (Alg.8 l.35-49) and F (= sum over T' of e, R8)
     const int32_t pc = ldv(&ctl->pcnt);
+    if (pc > 0) {
+      device_loop(d, grid, sm, clk, RK_STAGE2, L, true, true);
+      // ---- S_min (R19) = stage 1's final forward reach from {s} u Exc_S (h- < |V|)
+      //      united with the forward reach, inside P, of the excess left in P: no
+      //      residual edge enters P from S\P or leaves P towards T\P
+      if (blockIdx.x == 0 && threadIdx.x < NB) {
+        ctl->qc[threadIdx.x] = 0;
+        if (threadIdx.x < 2) { ctl->fs[threadIdx.x] = 0; ctl->mu[threadIdx.x] = 0; }
+      }
+      grid.sync();
+      device_loop(d, grid, sm, clk, RK_MINCUT_P, L, false, false);
+    }
+    // ---- relabel partitions (Alg.8 l.35-49) and F (= sum over T' of e, R8)
     for (int32_t x = gt; x < pc; x += nt) {
       const int32_t v = d.plist[x];
       d.part[v] = ldv(d.hp + v) < n ? PART_T : PART_S;
@@ -1162,6 +1179,7 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(Dev d, int32_t m
     for (int32_t v = gt; v < n; v += nt) {
       const long long ev = ldv(d.e + v);
       f += v == d.t ? ev : (v != d.s && ev < 0 ? ev : 0);
+      d.mask[v] = ldv(d.hm + v) < n ? 1 : 0;     // S_min, cached for dmf_min_cut_source_side
     }
     f = bg.sum(f);
     if (threadIdx.x == 0 && f) atomicAdd(reinterpret_cast<unsigned long long *>(&ctl->flow), (unsigned long long)f);

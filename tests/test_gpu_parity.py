@@ -258,19 +258,81 @@ def test_static_resolve_after_batches_matches(dmf):
 
 
 # ------------------------------------------------------------------ full-size configs
+# BASELINE.json configs 2-5 at full size, in the launch configuration bench.py times
+# (default grid, KERNELCYCLES = floor(m/n)).  F and S_min are compared bit-exactly
+# with the oracle (two-phase FIFO push-relabel) after the static solve and after
+# every batch; the exported state passes the checker where noted.
 
-@pytest.mark.full
-@pytest.mark.parametrize("algo", ["pp", "pr"])
-def test_rmat20_full(dmf, algo):
-    """Config 2 at full size (RMAT-20, 16M edges): static + 1%/0.1%/10% batches in
-    the bench's launch configuration; every state vs the oracle and the checker."""
-    g = W.config_graph("rmat20")
+def _full_run(dmf, g, batches, algos, check_states=(0,)):
     f = dmf.DynMaxFlow.from_graph(g)
     f.static_solve()
-    _verify(f, g, "rmat20 static")
     st = W.CapState(g)
-    for j, frac in enumerate([0.01, 0.001, 0.1]):
-        b = W.rmat_batch(g, st, frac, 100 + j)
+    _verify_full(f, g, "static", check=0 in check_states)
+    for j, (b, algo) in enumerate(zip(batches(st), algos)):
         st.apply(b)
         f.apply_batch(b.u, b.v, b.new_cap, algo=algo)
-        _verify(f, st.graph(), f"rmat20 b{j} {algo}")
+        _verify_full(f, st.graph(), f"b{j} {algo}", check=(j + 1) in check_states)
+    return f
+
+
+def _verify_full(f, g, tag, check):
+    r = O.maxflow(g, "fifo_pr")
+    F = f.flow_value()
+    assert F == r["F"], f"{tag}: F gpu={F} oracle={r['F']}"
+    smin = f.min_cut_source_side()
+    assert np.array_equal(smin, r["smin"]), f"{tag}: S_min differs ({int((smin != r['smin']).sum())} vertices)"
+    if check:
+        stt = f.export_state()
+        rc, msg, _ = O.check_state(g.n, g.s, g.t, stt["row_ptr"], stt["dst"], stt["rev"], stt["cap"], stt["res"],
+                                   stt["e"], F, smin)
+        assert rc == 0, f"{tag}: checker {rc}: {msg}"
+
+
+def _rmat_batches(g, fracs, seed0):
+    def gen(st):
+        for j, fr in enumerate(fracs):
+            b = W.rmat_batch(g, st, fr, seed0 + j)
+            yield b
+    return gen
+
+
+@pytest.mark.full
+def test_config2_rmat20_full(dmf):
+    """Config 2: RMAT-20 (1M / 16.1M), 1% / 0.1% / 10% mixed batches, PP and PR."""
+    g = W.config_graph("rmat20")
+    _full_run(dmf, g, _rmat_batches(g, [0.01, 0.001, 0.1, 0.01], 100), ["pp", "pr", "pp", "pr"], check_states=(0, 1))
+
+
+@pytest.mark.full
+def test_config3_grid2048_full(dmf):
+    """Config 3: 2048x2048 segmentation grid, terminal-capacity batches (0.1% / 1% of pixels)."""
+    g = W.config_graph("grid2048")
+
+    def gen(st):
+        for j, fr in enumerate([0.01, 0.001, 0.01]):
+            yield W.grid_batch(g, fr, 300 + j)
+    _full_run(dmf, g, gen, ["pr", "pp", "pp"], check_states=(1,))
+
+
+@pytest.mark.full
+def test_config4_bipartite_full(dmf):
+    """Config 4: unit bipartite 4M+4M / 72.7M merged edges; F = Hopcroft-Karp matching;
+    one 1% insert/delete batch with PP."""
+    g = W.config_graph("bip4m")
+    L = g.meta["L"]
+    a, b_ = g.meta["lr_begin"], g.meta["lr_end"]
+    lr = g.cap[a:b_] > 0
+    f = dmf.DynMaxFlow.from_graph(g)
+    assert f.static_solve() == O.hopcroft_karp(L, L, g.u[a:b_][lr], g.v[a:b_][lr] - L)
+    st = W.CapState(g)
+    b = W.bipartite_batch(g, st, 0.01, 400)
+    st.apply(b)
+    f.apply_batch(b.u, b.v, b.new_cap, algo="pp")
+    _verify_full(f, st.graph(), "bip b0 pp", check=False)
+
+
+@pytest.mark.full
+def test_config5_rmat22_snapshot_full(dmf):
+    """Config 5 (one snapshot per GPU): RMAT-22 (4.2M / 65.2M), 1% PP batches."""
+    g = W.config_graph("rmat22_1")
+    _full_run(dmf, g, _rmat_batches(g, [0.01, 0.01], 100), ["pp", "pp"], check_states=())
