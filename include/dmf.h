@@ -160,8 +160,8 @@ int dmf_get_stats(const dmf_graph *g, dmf_stats *out);
 /* Phase tracing (aux/debug): capacity > 0 allocates a device ring of `capacity`
  * records; every later call records one record per grid phase of its kernel:
  * {phase, iteration, level-or-round, items, extra, duration_ns} (int32 x 6) where
- * phase is 0 prologue, 1 reset, 2 bfs level, 3 discharge round, 4 rie,
- * 5 epilogue.  capacity = 0 disables tracing. */
+ * phase is 0 prologue, 1 reset, 2 bfs level expansion, 3 discharge round, 4 rie,
+ * 5 epilogue, 6 bfs bottom-up pass B, 7 bfs compaction.  capacity = 0 disables tracing. */
 int dmf_set_trace(dmf_graph *g, int32_t capacity);
 
 /* Copy the trace of the LAST call: *count = records written; up to `capacity`

@@ -217,7 +217,7 @@ class DynMaxFlow:
         self._check(self._L.dmf_get_stats(self._h, ctypes.byref(st)))
         return {f: getattr(st, f) for f, _ in Stats._fields_}
 
-    PHASES = {0: "prologue", 1: "reset", 2: "bfs", 3: "discharge", 4: "rie", 5: "epilogue"}
+    PHASES = {0: "prologue", 1: "reset", 2: "bfs", 3: "discharge", 4: "rie", 5: "epilogue", 6: "bfs_bu", 7: "bfs_cmp"}
 
     def set_trace(self, capacity: int = 4096):
         self._check(self._L.dmf_set_trace(self._h, int(capacity)))

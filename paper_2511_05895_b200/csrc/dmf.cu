@@ -277,7 +277,7 @@ static int run_solve(dmf_graph *g, int32_t mode, const Dev &dv) {
   st.bottom_up_levels = (int64_t)c.stat[ST_BU_LEVELS];
   st.t_prologue_us = c.stat[ST_T_PRO] * 1e-3f;
   st.t_reset_us = c.stat[ST_T_RESET] * 1e-3f;
-  st.t_bfs_us = c.stat[ST_T_BFS] * 1e-3f;
+  st.t_bfs_us = (c.stat[ST_T_BFS] + c.stat[ST_T_BFS_BU] + c.stat[ST_T_BFS_CMP]) * 1e-3f;
   st.t_discharge_us = c.stat[ST_T_DIS] * 1e-3f;
   st.t_rie_us = c.stat[ST_T_RIE] * 1e-3f;
   st.t_epilogue_us = c.stat[ST_T_EPI] * 1e-3f;

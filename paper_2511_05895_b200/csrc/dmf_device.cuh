@@ -41,7 +41,7 @@ enum Mode : int32_t {
 enum Stat : int {
   ST_ITERS, ST_LEVELS, ST_BFS_V, ST_BFS_SLOTS, ST_DIS_V, ST_DIS_SLOTS, ST_PUSHES,
   ST_RELABELS, ST_RIE_SLOTS, ST_RIE_SAT, ST_S2_V, ST_S2_ITERS, ST_ROUNDS, ST_ACTIVATIONS, ST_RESET_V, ST_BUDGET_STOPS, ST_BU_LEVELS,
-  ST_T_PRO, ST_T_RESET, ST_T_BFS, ST_T_DIS, ST_T_RIE, ST_T_EPI, ST_N
+  ST_T_PRO, ST_T_RESET, ST_T_BFS, ST_T_DIS, ST_T_RIE, ST_T_EPI, ST_T_BFS_BU, ST_T_BFS_CMP, ST_N
 };
 
 // Control block in device memory (zeroed by the host before every launch).

@@ -37,6 +37,17 @@ namespace dmf {
 
 constexpr int MAX_ROUNDS = 4096;  // hard cap of discharge rounds per global relabel
 
+// Block-staged appends (BFS): see stage_conv / stage_flush.
+constexpr int SF = 1024;            // staged entries per frontier bin (bins 0, 1)
+constexpr int SW = 256;             // staged entries per worklist bin (bins 0..3)
+
+struct Stage {
+  int32_t cnt[6];                   // 0,1: frontier bins 0,1; 2..5: worklist bins 0..3
+  int32_t base[6];
+  int32_t f[2][SF];
+  int32_t w[4][SW];
+};
+
 struct TileSm {
   int32_t cnt[8];
   int32_t base[8];
@@ -45,8 +56,9 @@ struct TileSm {
 struct Smem {
   long long red[WPB + 1];
   unsigned long long stat[ST_N];
-  TileSm ts;
   long long budget[WPB + 1];   // push budgets: one per warp group + one for the CTA group
+  Stage st;                    // block-staged appends (BFS)
+  TileSm ts;                   // tiled compaction (dense top-down BFS levels)
 };
 
 // Phase clock (block 0, thread 0): time between consecutive grid barriers is
@@ -198,81 +210,161 @@ __device__ __forceinline__ void activate(const Dev &d, const Track &k, const BL 
 
 // ---------------------------------------------------------------------------
 // BFS (global relabel).  Level-synchronous; per level and per
-// track it is either
+// track either
 //   top-down   the frontier's rows are scanned: a residual edge (v -> w) [push
 //              track] / (w -> v) [pull track] from frontier vertex w labels v, or
 //   bottom-up  every unlabelled vertex of the track's region looks for a residual
 //              edge into the frontier and stops at the first (direction-optimising
 //              BFS; chosen when the frontier's slots exceed 1/BU_ALPHA of the
 //              unlabelled vertices' slots).
-// and the next frontier / active worklist are built either
-//   SPARSE     claims by CAS and warp-aggregated appends inside the expansion (small
-//              frontiers: little contention), or
-//   DENSE      labels are plain idempotent stores h(v) = lvl+1 and a separate tiled
-//              compaction over the vertex domain builds the next frontier and the
-//              worklist with block-aggregated appends (ballot + one global atomic per
-//              list per 2048-vertex tile -- the paper's ballot worklist).
+// Region encoding: RESET gives vertices outside a track's region the height |V|+1,
+// so "unlabelled" (h == |V|) already means "in the region": one gather per slot.
+// Top-down claims are atomicCAS(h, |V|, lvl+1) (unique claimer); bottom-up claims
+// are plain stores (one examiner per vertex).  Claimed vertices are appended to the
+// next frontier and, if active, to the worklist through BLOCK-STAGED appends:
+// warp ballot + shared-memory reservation, flushed with one global atomic per list
+// per CTA at the end of the phase (the paper's ballot worklist).
 constexpr unsigned long long BU_ALPHA = 2;
-constexpr unsigned long long SPARSE_DIV = 64;     // sparse iff frontier slots < S / SPARSE_DIV
+constexpr unsigned long long DENSE_DIV = 64;      // top-down by stores + compaction iff frontier slots >= S/64
 constexpr int TILE_ITEMS = 4;                     // vertices per thread per compaction tile
 
 struct BfsCtx {
   int32_t lvl;
-  uint8_t reg0, reg1;
   bool collect;
   bool bu[2];                       // bottom-up this level, per track
-  bool sparse;                      // CAS + appends in the expansion
+  bool dense[2];                    // top-down by idempotent stores + compaction, per track
   BL next, wl;
   unsigned long long *fs_next;      // [2] slot counts of the next frontier per track
 };
 
-// ---- SPARSE claims -----------------------------------------------------------
-__device__ __forceinline__ void claim_append(const Dev &d, const BfsCtx &c, bool claimed, bool act, int32_t v, int tr) {
-  bl_append_conv(d, c.next, claimed && tr == 0, v, 0u);
-  bl_append_conv(d, c.next, claimed && tr == 1, v, TRACK_BIT);
-  if (c.collect) {
-    bl_append_conv(d, c.wl, act && tr == 0, v, 0u);
-    bl_append_conv(d, c.wl, act && tr == 1, v, TRACK_BIT);
+// ---- block-staged appends (Stage is declared with Smem above) ----------------------
+
+__device__ __forceinline__ int32_t *stage_buf(Stage &st, int k) { return k < 2 ? st.f[k] : st.w[k - 2]; }
+__device__ __forceinline__ int32_t stage_cap(int k) { return k < 2 ? SF : SW; }
+__device__ __forceinline__ void stage_target(const BL &next, const BL &wl, int k, int32_t *&list, int32_t *&cnt) {
+  if (k < 2) { list = next.bin(k); cnt = next.c + k; } else { list = wl.bin(k - 2); cnt = wl.c + (k - 2); }
+}
+
+// warp-convergent append of `val` into stage k (overflow goes straight to global)
+__device__ __forceinline__ void stage_conv(Stage &st, int k, int32_t *glist, int32_t *gcnt, bool pred, int32_t val) {
+  const unsigned m = __ballot_sync(0xffffffffu, pred);
+  if (m == 0) return;
+  const int lane = threadIdx.x & 31;
+  const int lead = __ffs(m) - 1;
+  int pos = 0;
+  if (lane == lead) pos = atomicAdd(&st.cnt[k], __popc(m));
+  pos = __shfl_sync(0xffffffffu, pos, lead) + __popc(m & ((1u << lane) - 1u));
+  const bool in_sm = pred && pos < stage_cap(k);
+  if (in_sm) stage_buf(st, k)[pos] = val;
+  warp_append(pred && !in_sm, val, glist, gcnt);
+}
+
+__device__ __forceinline__ void stage_one(Stage &st, int k, int32_t *glist, int32_t *gcnt, int32_t val) {
+  const int pos = atomicAdd(&st.cnt[k], 1);
+  if (pos < stage_cap(k)) { stage_buf(st, k)[pos] = val; return; }
+  glist[atomicAdd(gcnt, 1)] = val;
+}
+
+// block-wide: move the staged entries to their global lists (one atomic per list)
+__device__ __forceinline__ void stage_flush(Stage &st, const BL &next, const BL &wl) {
+  __syncthreads();
+  if (threadIdx.x < 6) {
+    const int k = threadIdx.x;
+    const int32_t c = min(st.cnt[k], stage_cap(k));
+    int32_t *list, *cnt;
+    stage_target(next, wl, k, list, cnt);
+    st.base[k] = c ? atomicAdd(cnt, c) : 0;
   }
-  const unsigned m = __ballot_sync(0xffffffffu, claimed);
-  if (m) {
-    const long long deg = claimed ? (long long)(d.row[v + 1] - d.row[v]) : 0;
+  __syncthreads();
+  for (int k = 0; k < 6; k++) {
+    const int32_t c = min(st.cnt[k], stage_cap(k));
+    if (c == 0) continue;
+    int32_t *list, *cnt;
+    stage_target(next, wl, k, list, cnt);
+    const int32_t *b = stage_buf(st, k);
+    for (int32_t i = threadIdx.x; i < c; i += NT) list[st.base[k] + i] = b[i];
+  }
+  __syncthreads();
+  if (threadIdx.x < 6) st.cnt[threadIdx.x] = 0;
+  __syncthreads();
+}
+
+__device__ __forceinline__ int front_bin(int32_t deg) { return deg <= BIN0_MAX ? 0 : (deg <= BIN1_MAX ? 1 : 2); }
+__device__ __forceinline__ int wl_bin(int32_t deg) {
+  return deg <= BIN0_MAX ? 0 : (deg <= BIN1_MAX ? 1 : (deg <= BIN2_MAX ? 2 : 3));
+}
+
+// warp-convergent: claimed vertex -> next frontier (+ worklist if active); counts
+// the claimed vertex's slots into fs[track]
+__device__ __noinline__ void claim_push(const Dev &d, Stage &st, const BfsCtx &c, bool claimed, bool act, int32_t v,
+                                           int tr, long long fs[2]) {
+  const int32_t deg = claimed ? d.row[v + 1] - d.row[v] : 0;
+  const int fb = claimed ? front_bin(deg) : -1;
+  const int32_t val = (int32_t)((uint32_t)v | (tr ? TRACK_BIT : 0u));
+  stage_conv(st, 0, c.next.bin(0), c.next.c, fb == 0, val);
+  stage_conv(st, 1, c.next.bin(1), c.next.c + 1, fb == 1, val);
+  if (__ballot_sync(0xffffffffu, fb == 2)) {          // big rows -> edge-balanced chunks
+    const int32_t nch = fb == 2 ? (deg + CH - 1) / CH : 0;
     WarpG g{(int)(threadIdx.x & 31)};
-    const long long d0 = g.sum(tr == 0 ? deg : 0), d1 = g.sum(tr == 1 ? deg : 0);
-    if (g.lane == 0) {
-      if (d0) atomicAdd(c.fs_next, (unsigned long long)d0);
-      if (d1) atomicAdd(c.fs_next + 1, (unsigned long long)d1);
-    }
+    long long tot;
+    const int32_t ex = (int32_t)g.exscan(nch, tot);
+    int32_t base = 0;
+    if (g.lane == 0) base = atomicAdd(c.next.c + 3, (int32_t)tot);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    for (int32_t k = 0; k < nch; k++) c.next.cq[base + ex + k] = chunk_entry(v, tr ? TRACK_BIT : 0u, k);
   }
+  if (c.collect) {
+    const int wb = act ? wl_bin(deg) : -1;
+#pragma unroll
+    for (int b = 0; b < 4; b++) stage_conv(st, 2 + b, c.wl.bin(b), c.wl.c + b, wb == b, val);
+  }
+  if (claimed) fs[tr] += deg;
+}
+
+// single-thread version (bottom-up pass B leaders)
+__device__ __forceinline__ void claim_one(const Dev &d, Stage &st, const BfsCtx &c, bool act, int32_t v, int tr,
+                                          long long fs[2]) {
+  const int32_t deg = d.row[v + 1] - d.row[v];
+  const int32_t val = (int32_t)((uint32_t)v | (tr ? TRACK_BIT : 0u));
+  const int fb = front_bin(deg);
+  if (fb < 2) stage_one(st, fb, c.next.bin(fb), c.next.c + fb, val);
+  else {
+    const int32_t nch = (deg + CH - 1) / CH;
+    const int32_t pos = atomicAdd(c.next.c + 3, nch);
+    for (int32_t k = 0; k < nch; k++) c.next.cq[pos + k] = chunk_entry(v, tr ? TRACK_BIT : 0u, k);
+  }
+  if (c.collect && act) {
+    const int wb = wl_bin(deg);
+    stage_one(st, 2 + wb, c.wl.bin(wb), c.wl.c + wb, val);
+  }
+  fs[tr] += deg;
+}
+
+__device__ __forceinline__ bool activity(const Dev &d, bool collect, int tr, int32_t v) {
+  if (!collect) return false;
+  const long long ev = ldv(d.e + v);
+  return tr ? (ev < 0) : (ev > 0);
 }
 
 // one scanned slot (rb = the track's BFS residual, v = head); warp-convergent
-__device__ __forceinline__ void td_slot(const Dev &d, const BfsCtx &c, int tr, int32_t rb, int32_t v) {
+__device__ __forceinline__ void td_slot(const Dev &d, Stage &st, const BfsCtx &c, int tr, int32_t rb, int32_t v,
+                                        long long fs[2]) {
   const Track k = make_track(d, tr);
-  const uint8_t reg = tr ? c.reg1 : c.reg0;
-  bool ok = false;
-  if (rb > 0 && v != k.excl) {
-    const int32_t h = ldv(k.hgt + v);
-    const uint8_t p = reg ? ldv(d.part + v) : 0;       // issued together with h
-    ok = h == d.n && (reg == 0 || p == reg);
+  bool claimed = false, act = false;
+  const bool ok = rb > 0 && v != k.excl && ldv(k.hgt + v) == d.n;
+  const bool dn = c.dense[tr];          // many discoverers per vertex: a store, deduplicated by compaction
+  if (dn && ok) k.hgt[v] = c.lvl + 1;
+  if (!dn && ok) {
+    claimed = atomicCAS(k.hgt + v, d.n, c.lvl + 1) == d.n;
+    if (claimed) act = activity(d, c.collect, tr, v);
   }
-  if (c.sparse) {
-    bool claimed = false, act = false;
-    if (ok) {
-      claimed = atomicCAS(k.hgt + v, d.n, c.lvl + 1) == d.n;
-      if (claimed && c.collect) {
-        const long long ev = ldv(d.e + v);
-        act = tr ? (ev < 0) : (ev > 0);
-      }
-    }
-    claim_append(d, c, claimed, act, v, tr);
-  } else if (ok) {
-    k.hgt[v] = c.lvl + 1;                              // idempotent: every writer writes lvl+1
-  }
+  if (__ballot_sync(0xffffffffu, !dn) == 0) return;   // whole warp dense: nothing to append here
+  claim_push(d, st, c, claimed, act, v, tr, fs);
 }
 
 // warp per frontier vertex (bin 1): coalesced scan of its row, 4 slots per lane per step
-__device__ __forceinline__ void td_vertex_warp(const Dev &d, Smem &sm, int32_t entry, const BfsCtx &c) {
+__device__ __forceinline__ void td_vertex_warp(const Dev &d, Smem &sm, Stage &st, int32_t entry, const BfsCtx &c,
+                                               long long fs[2]) {
   const int tr = ((uint32_t)entry & TRACK_BIT) ? 1 : 0;
   if (c.bu[tr]) return;
   const int lane = threadIdx.x & 31;
@@ -288,7 +380,7 @@ __device__ __forceinline__ void td_vertex_warp(const Dev &d, Smem &sm, int32_t e
       vv[j] = i < end ? d.dst[i] : 0;
     }
 #pragma unroll
-    for (int j = 0; j < 4; j++) td_slot(d, c, tr, rb[j], vv[j]);
+    for (int j = 0; j < 4; j++) td_slot(d, st, c, tr, rb[j], vv[j], fs);
   }
   if (lane == 0) {
     sstat_add(sm, ST_BFS_SLOTS, (unsigned long long)(end - beg));
@@ -297,7 +389,8 @@ __device__ __forceinline__ void td_vertex_warp(const Dev &d, Smem &sm, int32_t e
 }
 
 // warp per CH-slot chunk of a big frontier row (edge-balanced)
-__device__ __forceinline__ void td_chunk_warp(const Dev &d, Smem &sm, long long ce, const BfsCtx &c) {
+__device__ __forceinline__ void td_chunk_warp(const Dev &d, Smem &sm, Stage &st, long long ce, const BfsCtx &c,
+                                              long long fs[2]) {
   const uint32_t lo = (uint32_t)ce;
   const int tr = (lo & TRACK_BIT) ? 1 : 0;
   if (c.bu[tr]) return;
@@ -315,15 +408,15 @@ __device__ __forceinline__ void td_chunk_warp(const Dev &d, Smem &sm, long long 
       vv[j] = i < end ? d.dst[i] : 0;
     }
 #pragma unroll
-    for (int j = 0; j < 4; j++) td_slot(d, c, tr, rb[j], vv[j]);
+    for (int j = 0; j < 4; j++) td_slot(d, st, c, tr, rb[j], vv[j], fs);
   }
   if (lane == 0) sstat_add(sm, ST_BFS_SLOTS, (unsigned long long)(end - rb0));
 }
 
 // warp over up to 32 low-degree frontier vertices (bin 0): their rows are
 // concatenated and split evenly over the lanes (degree scan + shuffle search)
-__device__ __forceinline__ void td_small_chunk(const Dev &d, Smem &sm, const int32_t *list, int32_t x0, int32_t cnt,
-                                               const BfsCtx &c) {
+__device__ __forceinline__ void td_small_chunk(const Dev &d, Smem &sm, Stage &st, const int32_t *list, int32_t x0,
+                                               int32_t cnt, const BfsCtx &c, long long fs[2]) {
   const int lane = threadIdx.x & 31;
   int32_t entry = 0, beg = 0, deg = 0;
   if (lane < cnt) {
@@ -353,7 +446,7 @@ __device__ __forceinline__ void td_small_chunk(const Dev &d, Smem &sm, const int
     const int32_t i = bj + (k - oj);
     int32_t rb = 0, v = 0;
     if (k < total) { rb = ldv(make_track(d, tr).B + i); v = d.dst[i]; }
-    td_slot(d, c, tr, rb, v);
+    td_slot(d, st, c, tr, rb, v, fs);
   }
   if (lane == 0) {
     sstat_add(sm, ST_BFS_SLOTS, (unsigned long long)total);
@@ -364,25 +457,22 @@ __device__ __forceinline__ void td_small_chunk(const Dev &d, Smem &sm, const int
 // ---- bottom-up ----------------------------------------------------------------
 // Pass A (thread per vertex) settles low-degree candidates and queues the others
 // (degree-binned); pass B (after a grid barrier) scans the queued rows with a
-// warp / a CTA per vertex and group-wide early exit.  Labels are stores.
+// warp / a CTA per vertex and group-wide early exit.
 constexpr int32_t BU_THREAD_MAX = 16;
 
-__device__ __forceinline__ int bu_candidate(const Dev &d, const BfsCtx &c, int32_t v) {
-  if (c.bu[0] && v != d.s && ldv(d.hp + v) == d.n && (c.reg0 == 0 || ldv(d.part + v) == c.reg0)) return 0;
-  if (c.bu[1] && v != d.t && ldv(d.hm + v) == d.n && (c.reg1 == 0 || ldv(d.part + v) == c.reg1)) return 1;
-  return -1;
-}
-
-__device__ __forceinline__ void bfs_bottom_up_a(const Dev &d, Smem &sm, const BfsCtx &c, int32_t *bul, int32_t *bulc) {
+__device__ __forceinline__ void bfs_bottom_up_a(const Dev &d, Smem &sm, Stage &st, const BfsCtx &c, int32_t *bul,
+                                                int32_t *bulc, long long fs[2]) {
   const int32_t n = d.n;
   const int32_t nt = gridDim.x * NT;
   unsigned long long scanned = 0;
   for (int32_t b = blockIdx.x * NT + (threadIdx.x & ~31); b < n; b += nt) {
     const int32_t v = b + (threadIdx.x & 31);
-    bool q1 = false, q2 = false;
+    bool q1 = false, q2 = false, claimed = false, act = false;
     int tr = 0;
     if (v < n) {
-      const int cand = bu_candidate(d, c, v);
+      int cand = -1;
+      if (c.bu[0] && v != d.s && ldv(d.hp + v) == n) cand = 0;
+      else if (c.bu[1] && v != d.t && ldv(d.hm + v) == n) cand = 1;
       if (cand >= 0) {
         tr = cand;
         const int32_t beg = d.row[v], end = d.row[v + 1];
@@ -391,8 +481,7 @@ __device__ __forceinline__ void bfs_bottom_up_a(const Dev &d, Smem &sm, const Bf
           q2 = !q1;
         } else {
           const Track k = make_track(d, tr);
-          bool hit = false;
-          for (int32_t i0 = beg; i0 < end && !hit; i0 += 4) {
+          for (int32_t i0 = beg; i0 < end && !claimed; i0 += 4) {
             int32_t r[4], w[4];
 #pragma unroll
             for (int j = 0; j < 4; j++) {
@@ -401,13 +490,17 @@ __device__ __forceinline__ void bfs_bottom_up_a(const Dev &d, Smem &sm, const Bf
             }
 #pragma unroll
             for (int j = 0; j < 4; j++)
-              if (!hit && r[j] > 0 && ldv(k.hgt + w[j]) == c.lvl) hit = true;
+              if (!claimed && r[j] > 0 && ldv(k.hgt + w[j]) == c.lvl) claimed = true;
             scanned += 4;
           }
-          if (hit) k.hgt[v] = c.lvl + 1;
+          if (claimed) {
+            k.hgt[v] = c.lvl + 1;
+            act = activity(d, c.collect, tr, v);
+          }
         }
       }
     }
+    claim_push(d, st, c, claimed, act, v, tr, fs);
     const uint32_t tag = tr ? TRACK_BIT : 0u;
     warp_append(q1, (int32_t)((uint32_t)v | tag), bul, bulc);
     warp_append(q2, (int32_t)((uint32_t)v | tag), bul + n, bulc + 1);
@@ -416,7 +509,8 @@ __device__ __forceinline__ void bfs_bottom_up_a(const Dev &d, Smem &sm, const Bf
 }
 
 template <class G>
-__device__ __forceinline__ void bfs_bottom_up_b(const Dev &d, const G &g, Smem &sm, const BfsCtx &c, int32_t entry) {
+__device__ __forceinline__ void bfs_bottom_up_b(const Dev &d, const G &g, Smem &sm, Stage &st, const BfsCtx &c,
+                                                int32_t entry, long long fs[2]) {
   const int tr = ((uint32_t)entry & TRACK_BIT) ? 1 : 0;
   const int32_t v = (int32_t)((uint32_t)entry & ~TRACK_BIT);
   const Track k = make_track(d, tr);
@@ -439,7 +533,10 @@ __device__ __forceinline__ void bfs_bottom_up_b(const Dev &d, const G &g, Smem &
     if (g.any(hit)) { found = true; break; }
   }
   if (g.rank() == 0) {
-    if (found) k.hgt[v] = c.lvl + 1;
+    if (found) {
+      k.hgt[v] = c.lvl + 1;
+      claim_one(d, st, c, activity(d, c.collect, tr, v), v, tr, fs);
+    }
     sstat_add(sm, ST_BFS_SLOTS, scanned);
   }
 }
@@ -536,46 +633,68 @@ __device__ __forceinline__ void compact_domain(const Dev &d, TileSm &ts, int32_t
   }
 }
 
-// One BFS level (expansion; claims).  Ends after its grid barrier(s).
-__device__ __forceinline__ void bfs_expand_level(const Dev &d, cg::grid_group &grid, Smem &sm, const BL &cur,
-                                                 const int32_t c[NB], const BfsCtx &ctx, int32_t *bul, int32_t *bulc) {
+// block-wide: flush the stages and publish the per-CTA frontier slot sums
+__device__ __forceinline__ void bfs_flush(Smem &sm, Stage &st, const BfsCtx &c, long long fs[2]) {
+  stage_flush(st, c.next, c.wl);
+  BlockG bg{sm.red};
+  const long long f0 = bg.sum(fs[0]), f1 = bg.sum(fs[1]);
+  if (threadIdx.x == 0) {
+    if (f0) atomicAdd(c.fs_next, (unsigned long long)f0);
+    if (f1) atomicAdd(c.fs_next + 1, (unsigned long long)f1);
+  }
+}
+
+// One BFS level.  Ends after its grid barrier(s).
+__device__ __forceinline__ void bfs_expand_level(const Dev &d, cg::grid_group &grid, Smem &sm, Stage &st,
+                                                 PhaseClock &clk, int32_t it, const BL &cur, const int32_t c[NB],
+                                                 const BfsCtx &ctx, int32_t *bul, int32_t *bulc) {
   const bool bu = ctx.bu[0] || ctx.bu[1];
-  if (bu) bfs_bottom_up_a(d, sm, ctx, bul, bulc);
+  long long fs[2] = {0, 0};
+  if (bu) bfs_bottom_up_a(d, sm, st, ctx, bul, bulc, fs);
   if (!(ctx.bu[0] && ctx.bu[1])) {
     const int32_t gw = blockIdx.x * WPB + (threadIdx.x >> 5), nw = gridDim.x * WPB;
-    for (int32_t x = gw; x < c[3]; x += nw) td_chunk_warp(d, sm, cur.cq[x], ctx);
-    for (int32_t x = gw; x < c[1]; x += nw) td_vertex_warp(d, sm, cur.bin(1)[x], ctx);
+    for (int32_t x = gw; x < c[3]; x += nw) td_chunk_warp(d, sm, st, cur.cq[x], ctx, fs);
+    for (int32_t x = gw; x < c[1]; x += nw) td_vertex_warp(d, sm, st, cur.bin(1)[x], ctx, fs);
     const int32_t *b0 = cur.bin(0);
-    for (int32_t x = gw * 32; x < c[0]; x += nw * 32) td_small_chunk(d, sm, b0, x, min(32, c[0] - x), ctx);
+    for (int32_t x = gw * 32; x < c[0]; x += nw * 32) td_small_chunk(d, sm, st, b0, x, min(32, c[0] - x), ctx, fs);
   }
+  bfs_flush(sm, st, ctx, fs);
   grid.sync();
+  clk.lap(d, sm, ST_T_BFS, it, ctx.lvl, total(c), (ctx.bu[0] ? 1 : 0) | (ctx.bu[1] ? 2 : 0) | (c[3] << 3));
   if (bu) {
     const int32_t q1 = ldv(bulc), q2 = ldv(bulc + 1);
     if (q1 + q2 > 0) {
+      fs[0] = fs[1] = 0;
       {
         BlockG g{sm.red};
-        for (int32_t x = blockIdx.x; x < q2; x += gridDim.x) bfs_bottom_up_b(d, g, sm, ctx, bul[d.n + x]);
+        for (int32_t x = blockIdx.x; x < q2; x += gridDim.x) bfs_bottom_up_b(d, g, sm, st, ctx, bul[d.n + x], fs);
       }
       {
         WarpG g{(int)(threadIdx.x & 31)};
         const int32_t gw = blockIdx.x * WPB + (threadIdx.x >> 5), nw = gridDim.x * WPB;
-        for (int32_t x = gw; x < q1; x += nw) bfs_bottom_up_b(d, g, sm, ctx, bul[x]);
+        for (int32_t x = gw; x < q1; x += nw) bfs_bottom_up_b(d, g, sm, st, ctx, bul[x], fs);
       }
+      bfs_flush(sm, st, ctx, fs);
       grid.sync();
+      clk.lap(d, sm, ST_T_BFS_BU, it, ctx.lvl, q1 + q2, q2);
     }
   }
 }
 
 // ---------------------------------------------------------------------------
-// Discharge of one active vertex (Alg.2 / Alg.6): up to KERNELCYCLES cycles of
-// "find the lowest residual neighbour (h^, slot); push if h(u) > h^, else lift
-// h(u) = h^+1" (clamped to n, R4/R5; ties by slot index, R6).
-//  * A push cycle pushes to the successive lowest neighbours at height h^ in slot
-//    order until the excess is gone -- exactly the run of Alg.2 cycles that would
-//    follow with the heights as read.
-//  * The same pass records the lowest height among slots that stay residual, so if
-//    excess remains (every admissible slot saturated) the lift goes straight to that
-//    minimum + 1 and the next cycle pushes without a separate argmin scan.
+// Discharge of one active vertex (Alg.2 / Alg.6), up to KERNELCYCLES cycles.  A
+// cycle is ONE pass over u's residual slots:
+//  * push to every admissible slot (h(v) < h(u)) until the excess is gone.  With the
+//    exact BFS labels every admissible slot has h(v) = h(u)-1 = h^, the lowest
+//    residual neighbour, so this is the run of Alg.2 pushes to v^ (l.15-19) in one
+//    pass; the excess is a budget the lanes claim with
+//    shared-memory atomics (any order among equal heights, R6);
+//  * the same pass records the lowest height among slots left residual, so if excess
+//    remains (all admissible slots saturated) the lift (l.21) goes straight to that
+//    minimum + 1 (clamped to |V|, R4/R5) and the next cycle pushes again.
+// A vertex whose excess is drained stops; a later push into it re-queues it (the
+// excess crosses 0).  A vertex that spends all KERNELCYCLES while active re-queues
+// itself for the next round.
 template <class G>
 __device__ __forceinline__ void discharge(const Dev &d, const G &g, Smem &sm, int32_t entry, const BL &rl,
                                           const BL &nxt, unsigned long long *workc) {
@@ -587,57 +706,16 @@ __device__ __forceinline__ void discharge(const Dev &d, const G &g, Smem &sm, in
   const int32_t beg = d.row[u], end = d.row[u + 1];
   if (g.rank() == 0) { d.inq[u] = 0; __threadfence(); }
   int32_t hu = ldv(k.hgt + u);
-  int32_t hhat = -1;                   // current lowest residual-neighbour height (-1: unknown)
   bool relabelled = false;
   unsigned long long scanned = 0, pushes = 0, lifts = 0;
   long long eu = 0;
+  if (g.rank() == 0) eu = ldv(d.e + u) * k.sign;
+  eu = g.bcast(eu);
   int cyc = 0;
-  for (; cyc < d.kc; ++cyc) {
-    if (g.rank() == 0) eu = ldv(d.e + u) * k.sign;
-    eu = g.bcast(eu);
-    if (hu >= n || eu <= 0) break;
-    if (hhat < 0) {                      // argmin scan (Alg.2 l.6-14)
-      unsigned long long best = ~0ull;
-      for (int32_t i0 = beg + g.rank(); i0 < end; i0 += 4 * G::size) {
-        int32_t r[4], v[4];
-#pragma unroll
-        for (int j = 0; j < 4; j++) {   // independent loads first (ILP), then the gathers
-          const int32_t i = i0 + j * G::size;
-          r[j] = i < end ? ldv(k.F + i) : 0;
-          v[j] = i < end ? d.dst[i] : 0;
-        }
-#pragma unroll
-        for (int j = 0; j < 4; j++) {
-          if (r[j] > 0) {
-            const int32_t h = ldv(k.hgt + v[j]);
-            best = (unsigned long long)(uint32_t)h < best ? (unsigned long long)(uint32_t)h : best;
-          }
-        }
-      }
-      scanned += (unsigned long long)(end - beg);
-      best = g.min(best);
-      if (best == ~0ull) {               // no residual out-edge: h^ = inf -> |V| (R4)
-        hu = n;
-        if (g.rank() == 0) k.hgt[u] = n;
-        relabelled = true;
-        lifts++;
-        break;
-      }
-      hhat = (int32_t)best;
-    }
-    if (hu <= hhat) {                    // lift(u) (Alg.2 l.21), clamped to |V| (R5)
-      hu = hhat + 1 < n ? hhat + 1 : n;
-      if (g.rank() == 0) k.hgt[u] = hu;
-      relabelled = true;
-      lifts++;
-      continue;
-    }
-    // push(u, v^) at height h^ (Alg.2 l.15-19), batched: the excess is a budget the
-    // lanes claim with shared-memory atomics (pushes to equal-height neighbours in
-    // any order; R6's slot order only fixes a tie-break that F and S_min ignore)
+  long long *bud = G::size == 1 ? nullptr : (G::size == NT ? &sm.budget[WPB] : &sm.budget[threadIdx.x >> 5]);
+  for (; cyc < d.kc && hu < n && eu > 0; ++cyc) {
     long long remaining = eu;
     unsigned long long nmin = ~0ull;     // lowest height among slots left residual
-    long long *bud = G::size == 1 ? nullptr : (G::size == NT ? &sm.budget[WPB] : &sm.budget[threadIdx.x >> 5]);
     if (G::size > 1) {
       if (g.rank() == 0) *bud = eu;
       if (G::size == NT) __syncthreads(); else __syncwarp();
@@ -646,7 +724,7 @@ __device__ __forceinline__ void discharge(const Dev &d, const G &g, Smem &sm, in
       if (G::size == 1 ? remaining <= 0 : *((volatile long long *)bud) <= 0) break;
       int32_t r[4], v[4], h[4];
 #pragma unroll
-      for (int j = 0; j < 4; j++) {
+      for (int j = 0; j < 4; j++) {     // independent loads first (ILP), then the gathers
         const int32_t i = i0 + j * G::size;
         r[j] = i < end ? ldv(k.F + i) : 0;
         v[j] = i < end ? d.dst[i] : 0;
@@ -657,7 +735,7 @@ __device__ __forceinline__ void discharge(const Dev &d, const G &g, Smem &sm, in
       for (int j = 0; j < 4; j++) {
         if (r[j] <= 0) continue;
         long long take = 0;
-        if (h[j] == hhat) {
+        if (h[j] < hu) {
           long long old;
           if (G::size == 1) { old = remaining; remaining -= r[j]; }
           else old = (long long)atomicAdd(reinterpret_cast<unsigned long long *>(bud),
@@ -687,23 +765,31 @@ __device__ __forceinline__ void discharge(const Dev &d, const G &g, Smem &sm, in
       if (G::size == NT) __syncthreads(); else __syncwarp();
     }
     const long long done = eu - (remaining > 0 ? remaining : 0);
-    if (g.rank() == 0 && done > 0) atom_add(d.e + u, -done * k.sign);   // e(u) -= d
-    if (remaining > 0) {                 // every admissible slot saturated
-      nmin = g.min(nmin);
-      if (nmin == ~0ull) {               // nothing residual any more: lift to |V|
-        hu = n;
-        if (g.rank() == 0) k.hgt[u] = n;
-        relabelled = true;
-        lifts++;
-        break;
+    long long left = 0;                      // exact excess after our pushes (others may have added)
+    if (g.rank() == 0) {
+      if (done > 0) {
+        const long long old = (long long)atomicAdd(reinterpret_cast<unsigned long long *>(d.e + u),
+                                                   (unsigned long long)(-done * k.sign));   // e(u) -= d
+        left = old * k.sign - done;
+      } else {
+        left = ldv(d.e + u) * k.sign;
       }
-      hhat = (int32_t)nmin;              // next cycle lifts (if h(u) <= h^) or pushes at h^
-    } else {
-      hhat = -1;                         // excess gone; rescan if more arrives
+    }
+    left = g.bcast(left);
+    eu = left;
+    if (left <= 0) break;                    // drained
+    if (remaining <= 0) continue;            // excess arrived meanwhile: push again at the same height
+    nmin = g.min(nmin);                      // every admissible slot saturated: lift
+    const int32_t nh = nmin == ~0ull ? n : (int32_t)min((unsigned long long)n, nmin + 1);
+    if (nh > hu) {
+      hu = nh;
+      if (g.rank() == 0) k.hgt[u] = hu;
+      relabelled = true;
+      lifts++;
     }
   }
   if (g.rank() == 0) {
-    if (cyc == d.kc && hu < n && ldv(d.e + u) * k.sign > 0) activate(d, k, nxt, u, tag, sm);  // KC spent
+    if (cyc == d.kc && hu < n && eu > 0) activate(d, k, nxt, u, tag, sm);  // KERNELCYCLES spent
     if (relabelled && d.rlf[u] == 0) { d.rlf[u] = 1; bl_append_one(d, rl, u, tag); }
     atomicAdd(workc, scanned + 16ull * lifts + 16ull);
     sstat_add(sm, ST_DIS_V, 1);
@@ -829,8 +915,6 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
   Ctl *ctl = d.ctl;
   int32_t *qc = ctl->qc, *wlc = ctl->wlc, *rlc = ctl->rlc;
   const int32_t nt = gridDim.x * NT;
-  const uint8_t reg0 = kind == RK_PP ? PART_T : (kind == RK_STAGE2 ? PART_P : 0);
-  const uint8_t reg1 = kind == RK_PP ? PART_S : (kind == RK_MINCUT_P ? PART_P : 0);
   const bool use0 = kind != RK_MINCUT && kind != RK_MINCUT_P;
   const bool use1 = kind == RK_PP || kind == RK_MINCUT || kind == RK_MINCUT_P;
   const bool on_plist = kind == RK_STAGE2 || kind == RK_MINCUT_P;
@@ -844,14 +928,18 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
       if (threadIdx.x < 2) { ctl->fs[2 + threadIdx.x] = 0; ctl->bulc[threadIdx.x] = 0; }
     }
     const int32_t N = on_plist ? ldv(&ctl->pcnt) : n;
-    const int32_t *dom = on_plist ? d.plist : nullptr;
     {
-      long long fs0 = 0, fs1 = 0, mu0 = 0, mu1 = 0;
-      BL f0{L.q[0], qc, n, L.qc[0]};
-      compact_domain(d, sm.ts, N, dom, f0, BL{L.wl[0], wlc, n, nullptr}, false,
-        [&](int32_t v, int &tr, bool &front, bool &act) {
+      // heights: 0 for roots, |V| for the rest of the track's region, |V|+1 outside it
+      long long fs[2] = {0, 0}, mu0 = 0, mu1 = 0;
+      const BfsCtx c0{0, false, {false, false}, {false, false}, BL{L.q[0], qc, n, L.qc[0]},
+                      BL{L.wl[0], wlc, n, nullptr}, ctl->fs};
+      for (int32_t b = blockIdx.x * NT + (threadIdx.x & ~31); b < N; b += nt) {
+        const int32_t x = b + (threadIdx.x & 31);
+        bool r0 = false, r1 = false, in0 = false, in1 = false;
+        int32_t v = 0;
+        if (x < N) {
+          v = on_plist ? d.plist[x] : x;
           const long long ev = ldv(d.e + v);
-          bool r0 = false, r1 = false, in0 = false, in1 = false;
           if (kind == RK_PUSH || kind == RK_MAXCUT) {
             r0 = v == d.t || (v != d.s && ev < 0);
             in0 = v != d.s;
@@ -862,10 +950,10 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
             in1 = p == PART_S && v != d.t;
             r0 = in0 && (v == d.t || ev < 0);
             r1 = in1 && (v == d.s || ev > 0);
-            d.hp[v] = r0 ? 0 : n;
-            d.hm[v] = r1 ? 0 : n;
-          } else if (kind == RK_STAGE2) {
-            r0 = ev < 0;
+            d.hp[v] = r0 ? 0 : (in0 ? n : n + 1);
+            d.hm[v] = r1 ? 0 : (in1 ? n : n + 1);
+          } else if (kind == RK_STAGE2) {       // P only; outside P heights stay >= |V| or
+            r0 = ev < 0;                        // belong to T\P, which no P vertex reaches
             in0 = true;
             d.hp[v] = r0 ? 0 : n;
           } else if (kind == RK_MINCUT_P) {     // forward reach of the excess left in P
@@ -881,15 +969,13 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
             const long long deg = d.row[v + 1] - d.row[v];
             if (in0 && !r0) mu0 += deg; else mu1 += deg;
           }
-          front = r0 || r1;
-          tr = r1 ? 1 : 0;
-          act = false;
-        }, fs0, fs1);
+        }
+        claim_push(d, sm.st, c0, r0 || r1, false, v, r1 ? 1 : 0, fs);
+      }
+      bfs_flush(sm, sm.st, c0, fs);
       BlockG bg{sm.red};
-      fs0 = bg.sum(fs0); fs1 = bg.sum(fs1); mu0 = bg.sum(mu0); mu1 = bg.sum(mu1);
+      mu0 = bg.sum(mu0); mu1 = bg.sum(mu1);
       if (threadIdx.x == 0) {
-        if (fs0) atomicAdd(ctl->fs, (unsigned long long)fs0);
-        if (fs1) atomicAdd(ctl->fs + 1, (unsigned long long)fs1);
         if (mu0) atomicAdd(ctl->mu, (unsigned long long)mu0);
         if (mu1) atomicAdd(ctl->mu + 1, (unsigned long long)mu1);
       }
@@ -908,9 +994,9 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
       read_counts(cur_c, c);
       beacon(d, 20 + kind, iter, 0, lvl, total(c), c[3]);
       if (total(c) == 0) break;
-      unsigned long long *fs = ctl->fs + 2 * (lvl % 3);
-      const long long f0 = ldv(reinterpret_cast<const long long *>(fs));
-      const long long f1 = ldv(reinterpret_cast<const long long *>(fs + 1));
+      unsigned long long *fsl = ctl->fs + 2 * (lvl % 3);
+      const long long f0 = ldv(reinterpret_cast<const long long *>(fsl));
+      const long long f1 = ldv(reinterpret_cast<const long long *>(fsl + 1));
       if (lvl > 0) { mu[0] -= f0; mu[1] -= f1; }
       if (blockIdx.x == 0 && threadIdx.x < NB) {
         qc[NB * ((lvl + 2) % 3) + threadIdx.x] = 0;
@@ -921,33 +1007,31 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
       }
       const bool bu0 = f0 > 0 && (unsigned long long)f0 * BU_ALPHA > (unsigned long long)(mu[0] > 0 ? mu[0] : 0);
       const bool bu1 = f1 > 0 && (unsigned long long)f1 * BU_ALPHA > (unsigned long long)(mu[1] > 0 ? mu[1] : 0);
-      const bool sparse = !bu0 && !bu1 && (unsigned long long)(f0 + f1) * SPARSE_DIV < (unsigned long long)d.S;
-      const BL nextl{L.q[(lvl + 1) & 1], qc + NB * ((lvl + 1) % 3), n, L.qc[(lvl + 1) & 1]};
-      const BL wll{L.wl[0], wlc, n, nullptr};
-      BfsCtx ctx{lvl, reg0, reg1, collect, {bu0, bu1}, sparse, nextl, wll, ctl->fs + 2 * ((lvl + 1) % 3)};
+      const bool dn0 = !bu0 && f0 > 0 && (unsigned long long)f0 * DENSE_DIV >= (unsigned long long)d.S;
+      const bool dn1 = !bu1 && f1 > 0 && (unsigned long long)f1 * DENSE_DIV >= (unsigned long long)d.S;
+      const BfsCtx ctx{lvl, collect, {bu0, bu1}, {dn0, dn1},
+                       BL{L.q[(lvl + 1) & 1], qc + NB * ((lvl + 1) % 3), n, L.qc[(lvl + 1) & 1]},
+                       BL{L.wl[0], wlc, n, nullptr}, ctl->fs + 2 * ((lvl + 1) % 3)};
       if (lead && (bu0 || bu1)) sstat_add(sm, ST_BU_LEVELS, 1);
-      bfs_expand_level(d, grid, sm, BL{L.q[lvl & 1], cur_c, n, L.qc[lvl & 1]}, c, ctx, d.bul,
+      bfs_expand_level(d, grid, sm, sm.st, clk, iter, BL{L.q[lvl & 1], cur_c, n, L.qc[lvl & 1]}, c, ctx, d.bul,
                        ctl->bulc + 2 * (lvl & 1));
-      if (!sparse) {                                // DENSE: build level lvl+1 by compaction
-        long long fs0 = 0, fs1 = 0;
-        compact_domain(d, sm.ts, N, dom, nextl, wll, collect,
+      if (dn0 || dn1) {                             // dense top-down tracks: build lvl+1 by compaction
+        long long g0 = 0, g1 = 0;
+        compact_domain(d, sm.ts, N, on_plist ? d.plist : nullptr, ctx.next, ctx.wl, collect,
           [&](int32_t v, int &tr, bool &front, bool &act) {
-            if (use0 && ldv(d.hp + v) == lvl + 1) { tr = 0; front = true; }
-            else if (use1 && ldv(d.hm + v) == lvl + 1) { tr = 1; front = true; }
-            if (front && collect) {
-              const long long ev = ldv(d.e + v);
-              act = tr ? (ev < 0) : (ev > 0);
-            }
-          }, fs0, fs1);
+            if (dn0 && ldv(d.hp + v) == lvl + 1) { tr = 0; front = true; }
+            else if (dn1 && ldv(d.hm + v) == lvl + 1) { tr = 1; front = true; }
+            if (front) act = activity(d, collect, tr, v);
+          }, g0, g1);
         BlockG bg{sm.red};
-        fs0 = bg.sum(fs0); fs1 = bg.sum(fs1);
+        g0 = bg.sum(g0); g1 = bg.sum(g1);
         if (threadIdx.x == 0) {
-          if (fs0) atomicAdd(ctx.fs_next, (unsigned long long)fs0);
-          if (fs1) atomicAdd(ctx.fs_next + 1, (unsigned long long)fs1);
+          if (g0) atomicAdd(ctx.fs_next, (unsigned long long)g0);
+          if (g1) atomicAdd(ctx.fs_next + 1, (unsigned long long)g1);
         }
         grid.sync();
+        clk.lap(d, sm, ST_T_BFS_CMP, iter, lvl, N);
       }
-      clk.lap(d, sm, ST_T_BFS, iter, lvl, total(c), (bu0 ? 1 : 0) | (bu1 ? 2 : 0) | (sparse ? 4 : 0) | (c[3] << 3));
     }
     if (lead) sstat_add(sm, ST_LEVELS, (unsigned long long)lvl);
     {
@@ -1054,6 +1138,7 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(Dev d, int32_t m
   cg::grid_group grid = cg::this_grid();
   __shared__ Smem sm;
   for (int i = threadIdx.x; i < ST_N; i += NTHREADS) sm.stat[i] = 0;
+  if (threadIdx.x < 6) sm.st.cnt[threadIdx.x] = 0;
   __syncthreads();
   const int32_t n = d.n;
   const int32_t gt = blockIdx.x * NTHREADS + threadIdx.x, nt = gridDim.x * NTHREADS;
@@ -1148,7 +1233,7 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(Dev d, int32_t m
       const int32_t v = b + (threadIdx.x & 31);
       bool inP = false;
       if (v < n) {
-        inP = d.row[v + 1] > d.row[v] && ldv(d.hp + v) == n && ldv(d.hm + v) == n;
+        inP = d.row[v + 1] > d.row[v] && ldv(d.hp + v) >= n && ldv(d.hm + v) >= n;
         if (inP) d.part[v] = PART_P;
       }
       warp_append(inP, v, d.plist, &ctl->pcnt);
