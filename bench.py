@@ -233,13 +233,14 @@ def main():
     hmask = torch.empty(g.n, dtype=torch.uint8).pin_memory()
     torch.cuda.synchronize()
 
+    raw = [P.Stats() for _ in range(nb)]
+
     def step(j, host=False):
         u, v, c = (hbat if host else dbat)[j]
         f.apply_batch(u, v, c, algo=args.algo)
-        s1 = f.stats()
+        f.raw_stats(raw[j])                      # ctypes copy only; dicts are built after timing
         if not args.no_cut:
             f.min_cut_source_side(hmask if host else dmask)
-        return s1
 
     for j in range(Wm):
         step(j)
@@ -254,13 +255,9 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = f.stats()["kernel_launches"]
     e0.record(stream)
-    kernel_ms, alg_bytes, per = [], [], []
     k_tot = 0
     for j in range(Wm, Wm + K):
-        s1 = step(j)
-        kernel_ms.append(s1["device_ms"])
-        alg_bytes.append(algorithmic_bytes(s1, g.n))
-        per.append(s1)
+        step(j)
         k_tot += batches[j].k
     e1.record(stream)
     torch.cuda.synchronize()
@@ -268,6 +265,9 @@ def main():
         dist.barrier()
     elapsed_ms = e0.elapsed_time(e1)
     launches = f.stats()["kernel_launches"] - launches0
+    per = [P.DynMaxFlow.stats_to_dict(raw[j]) for j in range(Wm, Wm + K)]
+    kernel_ms = [p_["device_ms"] for p_ in per]
+    alg_bytes = [algorithmic_bytes(p_, g.n) for p_ in per]
 
     # ---- timed: end to end from pinned host buffers, F + mask back to the host
     if world > 1:

@@ -159,13 +159,15 @@ int dmf_get_stats(const dmf_graph *g, dmf_stats *out);
 
 /* Phase tracing (aux/debug): capacity > 0 allocates a device ring of `capacity`
  * records; every later call records one record per grid phase of its kernel:
- * {phase, iteration, level-or-round, items, extra, duration_ns} (int32 x 6) where
+ * {phase, iteration, level-or-round, items, extra, duration_ns, slow_ns, slow_info}
+ * (int32 x 8; slow_* = the slowest vertex discharge of the phase: ns and
+ * (degree << 8 | cycles)) where
  * phase is 0 prologue, 1 reset, 2 bfs level expansion, 3 discharge round, 4 rie,
  * 5 epilogue, 6 bfs bottom-up pass B, 7 bfs compaction.  capacity = 0 disables tracing. */
 int dmf_set_trace(dmf_graph *g, int32_t capacity);
 
 /* Copy the trace of the LAST call: *count = records written; up to `capacity`
- * records are copied to `records` (host or device, int32[6 * capacity]). */
+ * records are copied to `records` (host or device, int32[8 * capacity]). */
 int dmf_get_trace(const dmf_graph *g, int32_t *records, int32_t capacity, int32_t *count);
 
 /* Sizes: *n vertices, *S slots, *m merged input edges (any may be NULL). */

@@ -213,8 +213,16 @@ class DynMaxFlow:
         return out
 
     def stats(self) -> dict:
-        st = Stats()
+        return self.stats_to_dict(self.raw_stats())
+
+    def raw_stats(self, into: "Stats | None" = None) -> Stats:
+        """dmf_get_stats into a ctypes struct (cheap; convert later with stats_to_dict)."""
+        st = into if into is not None else Stats()
         self._check(self._L.dmf_get_stats(self._h, ctypes.byref(st)))
+        return st
+
+    @staticmethod
+    def stats_to_dict(st: Stats) -> dict:
         return {f: getattr(st, f) for f, _ in Stats._fields_}
 
     PHASES = {0: "prologue", 1: "reset", 2: "bfs", 3: "discharge", 4: "rie", 5: "epilogue", 6: "bfs_bu", 7: "bfs_cmp"}
@@ -226,12 +234,14 @@ class DynMaxFlow:
         """Per-phase records of the last call: dicts (phase, iter, sub, items, extra, us)."""
         cnt = ctypes.c_int32()
         self._check(self._L.dmf_get_trace(self._h, None, 0, ctypes.byref(cnt)))
-        buf = np.zeros(6 * max(cnt.value, 1), np.int32)
+        buf = np.zeros(8 * max(cnt.value, 1), np.int32)
         self._check(self._L.dmf_get_trace(self._h, _ptr(buf), cnt.value, ctypes.byref(cnt)))
         out = []
-        for r in buf[:6 * cnt.value].reshape(-1, 6):
+        for r in buf[:8 * cnt.value].reshape(-1, 8):
             out.append(dict(phase=self.PHASES.get(int(r[0]), int(r[0])), iter=int(r[1]), sub=int(r[2]),
-                            items=int(r[3]), extra=int(r[4]), us=float(r[5]) * 1e-3))
+                            items=int(r[3]), extra=int(r[4]), us=float(r[5]) * 1e-3,
+                            slow_us=float(np.uint32(r[6])) * 1e-3, slow_deg=int(np.uint32(r[7])) >> 8,
+                            slow_cyc=int(np.uint32(r[7])) & 255))
         return out
 
     def export_state(self) -> dict:

@@ -555,7 +555,7 @@ int dmf_set_trace(dmf_graph *g, int32_t capacity) {
   if (!g || capacity < 0) return fail(DMF_EINVAL, "bad arguments");
   if (g->trace) { g->release(g->trace); g->trace = nullptr; g->trace_cap = 0; }
   if (capacity > 0) {
-    g->trace = (int32_t *)g->alloc((size_t)capacity * 6 * sizeof(int32_t));
+    g->trace = (int32_t *)g->alloc((size_t)capacity * 8 * sizeof(int32_t));
     if (!g->trace) return fail(DMF_ENOMEM, "trace buffer allocation failed");
     g->trace_cap = capacity;
   }
@@ -569,7 +569,7 @@ int dmf_get_trace(const dmf_graph *g, int32_t *records, int32_t capacity, int32_
   *count = nrec;
   if (records && nrec) {
     const int32_t c = nrec < capacity ? nrec : capacity;
-    CK(cudaMemcpy(records, g->trace, (size_t)c * 6 * sizeof(int32_t), cudaMemcpyDefault));
+    CK(cudaMemcpy(records, g->trace, (size_t)c * 8 * sizeof(int32_t), cudaMemcpyDefault));
   }
   return DMF_OK;
 }

@@ -57,6 +57,8 @@ struct Ctl {
   int32_t pad;
   long long flow;       // F
   unsigned long long work[3];   // discharge work per round [round % 3]
+  unsigned long long slow;      // trace mode: slowest discharge since the last trace record
+  int32_t claim[9];             // dynamic work claims of a discharge round [round % 3][CTA/warp/tile]
   unsigned long long fs[6];     // frontier slot counts [level % 3][track] (direction-optimising BFS)
   int32_t bulc[4];              // bottom-up candidate queue counts [level & 1][warp/CTA bin]
   unsigned long long mu[2];     // slots of the still-unlabelled vertices per track (BFS direction choice)
@@ -130,6 +132,7 @@ __device__ __forceinline__ void atom_add(long long *p, long long x) {
 // All members of a group call every collective below the same number of times.
 struct ThreadG {
   static constexpr int size = 1;
+  __device__ void sync() const {}
   __device__ int rank() const { return 0; }
   __device__ unsigned long long min(unsigned long long x) const { return x; }
   __device__ long long sum(long long x) const { return x; }
@@ -141,6 +144,7 @@ struct ThreadG {
 struct WarpG {
   static constexpr int size = 32;
   int lane;
+  __device__ void sync() const { __syncwarp(); }
   __device__ int rank() const { return lane; }
   __device__ unsigned long long min(unsigned long long x) const {
 #pragma unroll
@@ -169,10 +173,38 @@ struct WarpG {
   }
 };
 
+// Sub-warp tile of W lanes (W = 8: four low-degree vertices per warp).  Tiles of a
+// warp may diverge; every collective names only the tile's lanes.
+template <int W>
+struct TileG {
+  static constexpr int size = W;
+  int lane;          // lane within the warp
+  unsigned mask;     // this tile's lanes
+  __device__ TileG(int l) : lane(l), mask(((1u << W) - 1u) << (l & ~(W - 1))) {}
+  __device__ void sync() const { __syncwarp(mask); }
+  __device__ int rank() const { return lane & (W - 1); }
+  __device__ unsigned long long min(unsigned long long x) const {
+#pragma unroll
+    for (int o = W / 2; o > 0; o >>= 1) {
+      unsigned long long y = __shfl_xor_sync(mask, x, o, W);
+      x = y < x ? y : x;
+    }
+    return x;
+  }
+  __device__ long long sum(long long x) const {
+#pragma unroll
+    for (int o = W / 2; o > 0; o >>= 1) x += __shfl_xor_sync(mask, x, o, W);
+    return x;
+  }
+  __device__ long long bcast(long long x) const { return __shfl_sync(mask, x, 0, W); }
+  __device__ bool any(bool p) const { return __any_sync(mask, p); }
+};
+
 // CTA group: needs WPB+1 long longs of shared scratch.
 struct BlockG {
   static constexpr int size = NT;
   long long *sm;   // shared scratch
+  __device__ void sync() const { __syncthreads(); }
   __device__ int rank() const { return threadIdx.x; }
   __device__ unsigned long long min(unsigned long long x) const {
     WarpG w{(int)(threadIdx.x & 31)};

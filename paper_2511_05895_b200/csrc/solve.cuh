@@ -56,7 +56,7 @@ struct TileSm {
 struct Smem {
   long long red[WPB + 1];
   unsigned long long stat[ST_N];
-  long long budget[WPB + 1];   // push budgets: one per warp group + one for the CTA group
+  long long budget[4 * WPB + 1];   // push budgets: one per sub-warp tile / warp + one for the CTA
   Stage st;                    // block-staged appends (BFS)
   TileSm ts;                   // tiled compaction (dense top-down BFS levels)
 };
@@ -96,8 +96,11 @@ __device__ void PhaseClock::lap(const Dev &d, Smem &sm, int which, int32_t it, i
     const unsigned long long now = gtimer();
     sm.stat[which] += now - t;
     if (d.trace && d.ctl->ntrace < d.trace_cap) {       // per-phase trace record (DMF_TRACE)
-      int32_t *rec = d.trace + 6 * d.ctl->ntrace++;
+      int32_t *rec = d.trace + 8 * d.ctl->ntrace++;
       rec[0] = which - ST_T_PRO; rec[1] = it; rec[2] = sub; rec[3] = items; rec[4] = extra; rec[5] = (int32_t)(now - t);
+      const unsigned long long sl = d.ctl->slow;        // slowest discharge of the phase (if any)
+      rec[6] = (int32_t)(sl >> 32); rec[7] = (int32_t)(sl & 0xffffffffu);
+      d.ctl->slow = 0;
     }
     t = now;
   }
@@ -179,10 +182,51 @@ __device__ __forceinline__ void process_bl(const BL &bl, const int32_t c[NB], Sm
     for (int32_t x = gw; x < c[1]; x += nw) fn(g, b[x]);
   }
   {
-    ThreadG g;
+    TileG<8> g((int)(threadIdx.x & 31));
     const int32_t *b = bl.bin(0);
-    const int32_t gt = blockIdx.x * NT + threadIdx.x, nt = gridDim.x * NT;
+    const int32_t gt = (blockIdx.x * NT + threadIdx.x) >> 3, nt = (gridDim.x * NT) >> 3;
     for (int32_t x = gt; x < c[0]; x += nt) fn(g, b[x]);
+  }
+}
+
+// Dynamic variant (discharge rounds): CTAs, warps and 8-lane tiles take the next
+// item from atomic claim counters `cl[0..2]` (zeroed by the caller's counter
+// discipline), so a CTA busy with a big vertex takes nothing else and idle groups
+// absorb the remaining items.
+template <class Fn>
+__device__ __forceinline__ void process_bl_dyn(const BL &bl, const int32_t c[NB], Smem &sm, int32_t *cl, Fn fn) {
+  {
+    BlockG g{sm.red};
+    const int32_t nbig = c[3] + c[2];
+    for (;;) {
+      long long x = 0;
+      if (threadIdx.x == 0) x = atomicAdd(cl, 1);
+      x = g.bcast(x);
+      if (x >= nbig) break;
+      fn(g, x < c[3] ? bl.bin(3)[x] : bl.bin(2)[x - c[3]]);
+    }
+  }
+  {
+    WarpG g{(int)(threadIdx.x & 31)};
+    const int32_t *b = bl.bin(1);
+    for (;;) {
+      int32_t x = 0;
+      if (g.lane == 0) x = atomicAdd(cl + 1, 1);
+      x = __shfl_sync(0xffffffffu, x, 0);
+      if (x >= c[1]) break;
+      fn(g, b[x]);
+    }
+  }
+  {
+    TileG<8> g((int)(threadIdx.x & 31));
+    const int32_t *b = bl.bin(0);
+    for (;;) {
+      int32_t x = 0;
+      if (g.rank() == 0) x = atomicAdd(cl + 2, 1);
+      x = __shfl_sync(g.mask, x, 0, 8);
+      if (x >= c[0]) break;
+      fn(g, b[x]);
+    }
   }
 }
 
@@ -202,8 +246,7 @@ __device__ __forceinline__ int32_t total(const int32_t c[NB]) {
 __device__ __forceinline__ void activate(const Dev &d, const Track &k, const BL &nxt, int32_t v, uint32_t tag,
                                          Smem &sm) {
   if (v == d.s || v == d.t) return;
-  if (ldv(k.hgt + v) >= d.n) return;
-  if (atomicCAS(d.inq + v, 0, 1) != 0) return;
+  if (atomicCAS(d.inq + v, 0, 1) != 0) return;     // (a vertex at height >= |V| exits at once)
   bl_append_one(d, nxt, v, tag);
   sstat_add(sm, ST_ACTIVATIONS, 1);
 }
@@ -705,6 +748,7 @@ __device__ __forceinline__ void discharge(const Dev &d, const G &g, Smem &sm, in
   const int32_t n = d.n;
   const int32_t beg = d.row[u], end = d.row[u + 1];
   if (g.rank() == 0) { d.inq[u] = 0; __threadfence(); }
+  const unsigned long long t_start = d.trace ? gtimer() : 0;
   int32_t hu = ldv(k.hgt + u);
   bool relabelled = false;
   unsigned long long scanned = 0, pushes = 0, lifts = 0;
@@ -712,13 +756,15 @@ __device__ __forceinline__ void discharge(const Dev &d, const G &g, Smem &sm, in
   if (g.rank() == 0) eu = ldv(d.e + u) * k.sign;
   eu = g.bcast(eu);
   int cyc = 0;
-  long long *bud = G::size == 1 ? nullptr : (G::size == NT ? &sm.budget[WPB] : &sm.budget[threadIdx.x >> 5]);
+  long long *bud = G::size == 1 ? nullptr
+                  : (G::size == NT ? &sm.budget[4 * WPB]
+                                   : &sm.budget[4 * (threadIdx.x >> 5) + (G::size < 32 ? (int)((threadIdx.x & 31) / G::size) : 0)]);
   for (; cyc < d.kc && hu < n && eu > 0; ++cyc) {
     long long remaining = eu;
     unsigned long long nmin = ~0ull;     // lowest height among slots left residual
     if (G::size > 1) {
       if (g.rank() == 0) *bud = eu;
-      if (G::size == NT) __syncthreads(); else __syncwarp();
+      g.sync();
     }
     for (int32_t i0 = beg + g.rank(); i0 < end; i0 += 4 * G::size) {
       if (G::size == 1 ? remaining <= 0 : *((volatile long long *)bud) <= 0) break;
@@ -731,38 +777,49 @@ __device__ __forceinline__ void discharge(const Dev &d, const G &g, Smem &sm, in
       }
 #pragma unroll
       for (int j = 0; j < 4; j++) h[j] = r[j] > 0 ? ldv(k.hgt + v[j]) : 0;
+      long long take[4];
 #pragma unroll
-      for (int j = 0; j < 4; j++) {
-        if (r[j] <= 0) continue;
-        long long take = 0;
-        if (h[j] < hu) {
+      for (int j = 0; j < 4; j++) {       // budget claims
+        take[j] = 0;
+        if (r[j] > 0 && h[j] < hu) {
           long long old;
           if (G::size == 1) { old = remaining; remaining -= r[j]; }
           else old = (long long)atomicAdd(reinterpret_cast<unsigned long long *>(bud),
                                           (unsigned long long)(-(long long)r[j]));
-          take = old < 0 ? 0 : (old < r[j] ? old : r[j]);
+          take[j] = old < 0 ? 0 : (old < r[j] ? old : r[j]);
         }
-        if (take > 0) {
+        if (r[j] > 0 && take[j] < r[j])
+          nmin = (unsigned long long)(uint32_t)h[j] < nmin ? (unsigned long long)(uint32_t)h[j] : nmin;
+      }
+      long long oe[4];
+#pragma unroll
+      for (int j = 0; j < 4; j++) {       // all pushes of the step issued before any result is used
+        oe[j] = 0;
+        if (take[j] > 0) {
           const int32_t i = i0 + j * G::size;
           const int32_t ri = d.rev[i];
-          atomicSub(k.F + i, (int32_t)take);       // c_f(u,v^) -= d
-          atomicSub(k.R + ri, (int32_t)take);      //   mirror
-          atomicAdd(k.F + ri, (int32_t)take);      // c_f(v^,u) += d
-          atomicAdd(k.R + i, (int32_t)take);       //   mirror
-          const long long oe = (long long)atomicAdd(reinterpret_cast<unsigned long long *>(d.e + v[j]),
-                                                    (unsigned long long)(take * k.sign));   // e(v^) += d
-          const long long eo = oe * k.sign;
-          if (eo <= 0 && eo + take > 0) activate(d, k, nxt, v[j], tag, sm);
+          atomicSub(k.F + i, (int32_t)take[j]);      // c_f(u,v^) -= d
+          atomicSub(k.R + ri, (int32_t)take[j]);     //   mirror
+          atomicAdd(k.F + ri, (int32_t)take[j]);     // c_f(v^,u) += d
+          atomicAdd(k.R + i, (int32_t)take[j]);      //   mirror
+          oe[j] = (long long)atomicAdd(reinterpret_cast<unsigned long long *>(d.e + v[j]),
+                                       (unsigned long long)(take[j] * k.sign));   // e(v^) += d
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        if (take[j] > 0) {
+          const long long eo = oe[j] * k.sign;
+          if (eo <= 0 && eo + take[j] > 0) activate(d, k, nxt, v[j], tag, sm);
           pushes++;
         }
-        if (take < r[j]) nmin = (unsigned long long)(uint32_t)h[j] < nmin ? (unsigned long long)(uint32_t)h[j] : nmin;
       }
     }
     scanned += (unsigned long long)(end - beg);
     if (G::size > 1) {
-      if (G::size == NT) __syncthreads(); else __syncwarp();
+      g.sync();
       remaining = *bud;
-      if (G::size == NT) __syncthreads(); else __syncwarp();
+      g.sync();
     }
     const long long done = eu - (remaining > 0 ? remaining : 0);
     long long left = 0;                      // exact excess after our pushes (others may have added)
@@ -789,6 +846,12 @@ __device__ __forceinline__ void discharge(const Dev &d, const G &g, Smem &sm, in
     }
   }
   if (g.rank() == 0) {
+    if (d.trace) {                      // slowest discharge of the round: (ns, degree, cycles)
+      const unsigned long long dt = gtimer() - t_start;
+      const unsigned long long key = (min(dt, 0xffffffffull) << 32) |
+                                     ((unsigned long long)min(end - beg, 0xffffff) << 8) | (unsigned long long)min(cyc, 255);
+      atomicMax(&d.ctl->slow, key);
+    }
     if (cyc == d.kc && hu < n && eu > 0) activate(d, k, nxt, u, tag, sm);  // KERNELCYCLES spent
     if (relabelled && d.rlf[u] == 0) { d.rlf[u] = 1; bl_append_one(d, rl, u, tag); }
     atomicAdd(workc, scanned + 16ull * lifts + 16ull);
@@ -1060,11 +1123,12 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
       beacon(d, 30 + kind, iter, r, 0, total(w), w[3]);
       if (blockIdx.x == 0 && threadIdx.x < NB) {
         wlc[NB * nn + threadIdx.x] = 0;           // last read in round r-1 (before its barrier)
+        if (threadIdx.x < 3) ctl->claim[3 * nn + threadIdx.x] = 0;   // claimed in round r-1
         if (threadIdx.x == 0) ctl->work[nx] = 0;  // last read at the end of round r-2; filled in round r+1
       }
       const BL nxt{L.wl[(r + 1) & 1], wlc + NB * nx, n, nullptr};
-      process_bl(BL{L.wl[r & 1], wlc + NB * cur, n, nullptr}, w, sm,
-                 [&](auto &g, int32_t entry) { discharge(d, g, sm, entry, rl, nxt, ctl->work + cur); });
+      process_bl_dyn(BL{L.wl[r & 1], wlc + NB * cur, n, nullptr}, w, sm, ctl->claim + 3 * cur,
+                     [&](auto &g, int32_t entry) { discharge(d, g, sm, entry, rl, nxt, ctl->work + cur); });
       if (lead) sstat_add(sm, ST_ROUNDS, 1);
       grid.sync();
       clk.lap(d, sm, ST_T_DIS, iter, r, total(w), w[3]);
@@ -1089,6 +1153,7 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
     // ---------------- RIE over the vertices relabelled in this iteration
     if (blockIdx.x == 0 && threadIdx.x < NB) {
       for (int q = 0; q < 3; q++) wlc[NB * q + threadIdx.x] = 0;
+      if (threadIdx.x < 3) for (int q = 0; q < 3; q++) ctl->claim[3 * q + threadIdx.x] = 0;
       qc[threadIdx.x] = 0;                        // for the next RESET
       if (threadIdx.x < 2) { ctl->fs[threadIdx.x] = 0; ctl->mu[threadIdx.x] = 0; }
     }

@@ -23,4 +23,5 @@ for j in range(nb):
         for r in f.trace():
             ex = r['extra']
             extra = f"bu={ex & 3} sp={(ex >> 2) & 1} ch={ex >> 3}" if r['phase'] == 'bfs' else f"x={ex}"
-            print(f"  {r['phase']:9s} it={r['iter']:<3d} sub={r['sub']:<4d} items={r['items']:<9d} {extra:18s} {r['us']:9.1f} us")
+            sl = f"  slowest {r['slow_us']:.1f}us deg={r['slow_deg']} cyc={r['slow_cyc']}" if r['phase'] == 'discharge' else ""
+            print(f"  {r['phase']:9s} it={r['iter']:<3d} sub={r['sub']:<4d} items={r['items']:<9d} {extra:18s} {r['us']:9.1f} us{sl}")
