@@ -1232,39 +1232,41 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(Dev d, int32_t m
     }
     grid.sync();
     if (ldv(&ctl->status) != 0) mode = -1;       // all-or-nothing: state untouched
-    for (int64_t j = gt; mode >= 0 && j < d.k; j += nt) {   // Alg.5 l.1-3: c_f += c' - c
+    // Alg.5 l.1-3 (c_f += c' - c) and l.4-11 (a negative slot returns its excess flow:
+    // e(u) += d, e(v) -= d, R10) fused per entry: the clamp of slot i depends only on
+    // c_f(i) + delta_i (the entry of the reverse slot never changes c_f(i) unless it
+    // is the negative one, and a pair has at most one: their sum c'_i + c'_ri >= 0);
+    // all updates are commutative atomics.  DYN_PP also saturates a touched S->T slot
+    // here (Alg.8 l.10-13, R12): at a converged cut a T->S slot can never go negative,
+    // so nothing else changes such a slot in this phase.
+    for (int64_t j = gt; mode >= 0 && j < d.k; j += nt) {
       const int32_t i = d.bslot[j];
+      const int32_t ri = d.rev[i];
+      const int32_t u = d.bu[j], v = d.bv[j];
       const int32_t delta = d.bc[j] - d.cap[i];
-      d.res[i] += delta;
-      d.rres[d.rev[i]] += delta;
       d.cap[i] = d.bc[j];
-    }
-    if (mode >= 0) grid.sync();
-    for (int64_t j = gt; mode >= 0 && j < d.k; j += nt) {   // Alg.5 l.4-11 on touched slots only (R10)
-      const int32_t i = d.bslot[j];
-      const int32_t r = ldv(d.res + i);
-      if (r < 0) {
-        const int32_t ri = d.rev[i];
-        d.res[i] = 0;
-        d.rres[ri] = 0;
-        atomicAdd(d.res + ri, r);                 // c_f(v,u) += c_f(u,v)  (r < 0)
+      int32_t r = atomicAdd(d.res + i, delta) + delta;
+      atomicAdd(d.rres + ri, delta);
+      if (r < 0) {                                 // flow on (u,v) above the new capacity
+        const int32_t dd = -r;
+        atomicAdd(d.res + i, dd);
+        atomicAdd(d.rres + ri, dd);
+        atomicAdd(d.res + ri, -dd);
+        atomicAdd(d.rres + i, -dd);
+        atom_add(d.e + u, (long long)dd);
+        atom_add(d.e + v, -(long long)dd);
+        r = 0;
+      }
+      if (mode == MODE_PP && r > 0 && d.part[u] == PART_S && d.part[v] == PART_T) {
+        atomicAdd(d.res + i, -r);                  // saturate the touched S->T slot
+        atomicAdd(d.rres + ri, -r);
+        atomicAdd(d.res + ri, r);
         atomicAdd(d.rres + i, r);
-        atom_add(d.e + d.bu[j], -(long long)r);   // flow on (u,v) drops by -r: e(u) += -r
-        atom_add(d.e + d.bv[j], (long long)r);    //                           e(v) -= -r
+        atom_add(d.e + v, (long long)r);
+        atom_add(d.e + u, -(long long)r);
       }
     }
     if (mode >= 0) grid.sync();
-    if (mode == MODE_PP) {                        // Alg.8 l.10-13 on touched slots (R12)
-      for (int64_t j = gt; j < d.k; j += nt) {
-        const int32_t i = d.bslot[j];
-        const int32_t u = d.bu[j], v = d.bv[j];
-        if (d.part[u] == PART_S && d.part[v] == PART_T) {
-          const long long r = saturate_slot(d, i);
-          if (r) atom_add(d.e + u, -r);
-        }
-      }
-      grid.sync();
-    }
   }
   if (mode == MODE_STATIC || mode == MODE_PR) {
     // Alg.1 l.9-13 / Alg.4 l.3-8 (R3): saturate every residual out-slot of s
