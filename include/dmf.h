@@ -170,6 +170,13 @@ int dmf_set_trace(dmf_graph *g, int32_t capacity);
  * records are copied to `records` (host or device, int32[8 * capacity]). */
 int dmf_get_trace(const dmf_graph *g, int32_t *records, int32_t capacity, int32_t *count);
 
+/* Per-CTA view of the same trace (load-balance diagnostics): for record r and CTA b,
+ * busy_ns[r * grid + b] = ns from CTA b's previous grid-barrier exit to its arrival
+ * at the barrier that ends record r's phase.  *grid = CTAs of the persistent kernel;
+ * up to `capacity` records are copied (busy_ns: host or device, uint32[capacity *
+ * grid]; NULL only queries *grid). */
+int dmf_get_trace_cta(const dmf_graph *g, uint32_t *busy_ns, int32_t capacity, int32_t *grid);
+
 /* Sizes: *n vertices, *S slots, *m merged input edges (any may be NULL). */
 int dmf_sizes(const dmf_graph *g, int32_t *n, int64_t *S, int64_t *m);
 

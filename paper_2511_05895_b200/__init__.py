@@ -84,12 +84,13 @@ def load_library():
         L.dmf_export_state.argtypes = [P, P, P, P, P, P, P]
         L.dmf_set_trace.argtypes = [P, I32]
         L.dmf_get_trace.argtypes = [P, P, I32, ctypes.POINTER(I32)]
+        L.dmf_get_trace_cta.argtypes = [P, P, I32, ctypes.POINTER(I32)]
         L.dmf_destroy.argtypes = [P]
         L.dmf_destroy.restype = None
         L.dmf_last_error.restype = ctypes.c_char_p
         for f in ("dmf_create", "dmf_static_solve", "dmf_apply_batch", "dmf_flow_value", "dmf_min_cut_source_side",
                   "dmf_max_cut_source_side", "dmf_get_stats", "dmf_sizes", "dmf_export_state", "dmf_set_trace",
-                  "dmf_get_trace"):
+                  "dmf_get_trace", "dmf_get_trace_cta"):
             getattr(L, f).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -243,6 +244,16 @@ class DynMaxFlow:
                             slow_us=float(np.uint32(r[6])) * 1e-3, slow_deg=int(np.uint32(r[7])) >> 8,
                             slow_cyc=int(np.uint32(r[7])) & 255))
         return out
+
+    def trace_cta(self) -> np.ndarray:
+        """Per-CTA busy time (us) of every trace record of the last call: [records, grid]."""
+        cnt = ctypes.c_int32()
+        self._check(self._L.dmf_get_trace(self._h, None, 0, ctypes.byref(cnt)))
+        grid = ctypes.c_int32()
+        self._check(self._L.dmf_get_trace_cta(self._h, None, 0, ctypes.byref(grid)))
+        buf = np.zeros(max(cnt.value, 1) * grid.value, np.uint32)
+        self._check(self._L.dmf_get_trace_cta(self._h, _ptr(buf), cnt.value, ctypes.byref(grid)))
+        return buf[:cnt.value * grid.value].reshape(cnt.value, grid.value).astype(np.float64) * 1e-3
 
     def export_state(self) -> dict:
         row_ptr = np.zeros(self.n + 1, np.int64)

@@ -73,6 +73,7 @@ struct dmf_graph {
   Ctl *hctl = nullptr;       // pinned mirror
   int32_t *hdbg = nullptr;   // mapped pinned beacon (host view)
   int32_t *trace = nullptr;  // device trace ring (DMF_TRACE / dmf_set_trace)
+  uint32_t *trace_cta = nullptr;  // per-record per-CTA busy times (dmf_set_trace)
   int32_t trace_cap = 0;
   int32_t *ddbg = nullptr;   // device view
   int grid_blocks = 0;
@@ -222,6 +223,7 @@ static Dev make_dev(dmf_graph *g) {
   d.mask = g->mask; d.ctl = g->ctl;
   d.dbg = g->ddbg;
   d.trace = g->trace;
+  d.trace_cta = g->trace_cta;
   d.trace_cap = g->trace_cap;
   return d;
 }
@@ -554,9 +556,11 @@ int dmf_set_trace(dmf_graph *g, int32_t capacity) {
   g_last_error.clear();
   if (!g || capacity < 0) return fail(DMF_EINVAL, "bad arguments");
   if (g->trace) { g->release(g->trace); g->trace = nullptr; g->trace_cap = 0; }
+  if (g->trace_cta) { g->release(g->trace_cta); g->trace_cta = nullptr; }
   if (capacity > 0) {
     g->trace = (int32_t *)g->alloc((size_t)capacity * 8 * sizeof(int32_t));
-    if (!g->trace) return fail(DMF_ENOMEM, "trace buffer allocation failed");
+    g->trace_cta = (uint32_t *)g->alloc((size_t)capacity * g->grid_blocks * sizeof(uint32_t));
+    if (!g->trace || !g->trace_cta) return fail(DMF_ENOMEM, "trace buffer allocation failed");
     g->trace_cap = capacity;
   }
   return DMF_OK;
@@ -570,6 +574,18 @@ int dmf_get_trace(const dmf_graph *g, int32_t *records, int32_t capacity, int32_
   if (records && nrec) {
     const int32_t c = nrec < capacity ? nrec : capacity;
     CK(cudaMemcpy(records, g->trace, (size_t)c * 8 * sizeof(int32_t), cudaMemcpyDefault));
+  }
+  return DMF_OK;
+}
+
+int dmf_get_trace_cta(const dmf_graph *g, uint32_t *busy_ns, int32_t capacity, int32_t *grid) {
+  g_last_error.clear();
+  if (!g || !grid) return fail(DMF_EINVAL, "bad arguments");
+  *grid = g->grid_blocks;
+  const int32_t nrec = g->trace ? (g->hctl->ntrace < g->trace_cap ? g->hctl->ntrace : g->trace_cap) : 0;
+  if (busy_ns && nrec) {
+    const int32_t c = nrec < capacity ? nrec : capacity;
+    CK(cudaMemcpy(busy_ns, g->trace_cta, (size_t)c * g->grid_blocks * sizeof(uint32_t), cudaMemcpyDefault));
   }
   return DMF_OK;
 }

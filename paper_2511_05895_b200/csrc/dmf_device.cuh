@@ -99,7 +99,8 @@ struct Dev {
   uint8_t *mask;             // cut output
   Ctl *ctl;
   volatile int32_t *dbg;     // mapped pinned host words: progress beacon for the host watchdog
-  int32_t *trace;            // per-phase trace records (6 ints each), NULL unless tracing
+  int32_t *trace;            // per-phase trace records (8 ints each), NULL unless tracing
+  uint32_t *trace_cta;       // per-phase, per-CTA busy time (ns from the CTA's previous barrier exit to its arrival)
   int32_t trace_cap;
 };
 
@@ -123,6 +124,13 @@ __device__ __forceinline__ void beacon(const Dev &d, int32_t phase, int32_t iter
 __device__ __forceinline__ int32_t ldv(const int32_t *p) { return __ldcg(p); }
 __device__ __forceinline__ long long ldv(const long long *p) { return __ldcg(p); }
 __device__ __forceinline__ uint8_t ldv(const uint8_t *p) { return __ldcg(p); }
+// L1-allocating load, for data that no thread of the grid changes in the current
+// phase in a way the reader must observe (or whose stale values are harmless by
+// construction).  Safe across phases: the grid barrier's ld.acquire.gpu + CTA
+// barrier (cooperative_groups sync_grids_wait) orders the SM's later weak loads
+// after every write made before the barrier, so no stale L1 line survives it.
+__device__ __forceinline__ int32_t ldl1(const int32_t *p) { return __ldca(p); }
+__device__ __forceinline__ uint32_t ldl1(const uint32_t *p) { return __ldca(p); }
 __device__ __forceinline__ void atom_add(long long *p, long long x) {
   atomicAdd(reinterpret_cast<unsigned long long *>(p), static_cast<unsigned long long>(x));
 }

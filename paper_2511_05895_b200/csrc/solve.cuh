@@ -57,15 +57,20 @@ struct Smem {
   long long red[WPB + 1];
   unsigned long long stat[ST_N];
   long long budget[4 * WPB + 1];   // push budgets: one per sub-warp tile / warp + one for the CTA
+  unsigned long long work;         // discharge work of this CTA in the current round
+  unsigned long long tprev;        // trace mode: this CTA's last barrier exit
+  unsigned long long tclk;         // PhaseClock: block 0's last lap
+  long long cv[8];                 // control words snapped once per CTA (cta_snap)
   Stage st;                    // block-staged appends (BFS)
   TileSm ts;                   // tiled compaction (dense top-down BFS levels)
 };
 
 // Phase clock (block 0, thread 0): time between consecutive grid barriers is
 // charged to the phase that just ran.
+// (Stateless: the timestamp lives in shared memory, so no thread keeps a clock
+// object in local memory.)
 struct PhaseClock {
-  unsigned long long t;
-  __device__ void start() { if (blockIdx.x == 0 && threadIdx.x == 0) t = gtimer(); }
+  __device__ void start(Smem &sm) { if (blockIdx.x == 0 && threadIdx.x == 0) sm.tclk = gtimer(); }
   __device__ void lap(const Dev &d, Smem &sm, int which, int32_t it = 0, int32_t sub = 0, int32_t items = 0,
                       int32_t extra = 0);
 };
@@ -94,6 +99,7 @@ __device__ void PhaseClock::lap(const Dev &d, Smem &sm, int which, int32_t it, i
                                 int32_t extra) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     const unsigned long long now = gtimer();
+    const unsigned long long t = sm.tclk;
     sm.stat[which] += now - t;
     if (d.trace && d.ctl->ntrace < d.trace_cap) {       // per-phase trace record (DMF_TRACE)
       int32_t *rec = d.trace + 8 * d.ctl->ntrace++;
@@ -102,8 +108,22 @@ __device__ void PhaseClock::lap(const Dev &d, Smem &sm, int which, int32_t it, i
       rec[6] = (int32_t)(sl >> 32); rec[7] = (int32_t)(sl & 0xffffffffu);
       d.ctl->slow = 0;
     }
-    t = now;
+    sm.tclk = now;
   }
+}
+
+// Grid barrier.  In trace mode every CTA records how long it was busy in the phase
+// that ends here (load-balance / tail diagnostics, dmf_get_trace_cta).
+__device__ __forceinline__ void gsync(const Dev &d, cg::grid_group &grid, Smem &sm) {
+  if (d.trace_cta) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int32_t rec = ldv(&d.ctl->ntrace);
+      if (rec < d.trace_cap) d.trace_cta[(size_t)rec * gridDim.x + blockIdx.x] = (uint32_t)(gtimer() - sm.tprev);
+    }
+  }
+  grid.sync();
+  if (d.trace_cta && threadIdx.x == 0) sm.tprev = gtimer();
 }
 
 __device__ __forceinline__ int bin_of(const Dev &d, int32_t v) {
@@ -189,45 +209,71 @@ __device__ __forceinline__ void process_bl(const BL &bl, const int32_t c[NB], Sm
   }
 }
 
-// Dynamic variant (discharge rounds): CTAs, warps and 8-lane tiles take the next
-// item from atomic claim counters `cl[0..2]` (zeroed by the caller's counter
-// discipline), so a CTA busy with a big vertex takes nothing else and idle groups
-// absorb the remaining items.
+// Dynamic variant (discharge rounds): every CTA, warp and 8-lane tile takes its
+// first item statically (group id) and the next ones from atomic claim counters
+// `cl[0..2]` (zeroed by the caller's counter discipline), so a CTA busy with a big
+// vertex takes nothing else and idle groups absorb the remaining items.  A group
+// claims only after finishing an item: a near-empty round costs no claims (one
+// single-address atomic per group would serialise ~19k tile claims at L2).
 template <class Fn>
 __device__ __forceinline__ void process_bl_dyn(const BL &bl, const int32_t c[NB], Smem &sm, int32_t *cl, Fn fn) {
   {
     BlockG g{sm.red};
     const int32_t nbig = c[3] + c[2];
-    for (;;) {
-      long long x = 0;
-      if (threadIdx.x == 0) x = atomicAdd(cl, 1);
-      x = g.bcast(x);
-      if (x >= nbig) break;
+    long long x = blockIdx.x;
+    while (x < nbig) {
       fn(g, x < c[3] ? bl.bin(3)[x] : bl.bin(2)[x - c[3]]);
+      if (threadIdx.x == 0) x = (long long)gridDim.x + atomicAdd(cl, 1);
+      x = g.bcast(x);
     }
   }
   {
     WarpG g{(int)(threadIdx.x & 31)};
     const int32_t *b = bl.bin(1);
-    for (;;) {
-      int32_t x = 0;
-      if (g.lane == 0) x = atomicAdd(cl + 1, 1);
-      x = __shfl_sync(0xffffffffu, x, 0);
-      if (x >= c[1]) break;
+    const int32_t nw = gridDim.x * WPB;
+    int32_t x = blockIdx.x * WPB + (threadIdx.x >> 5);
+    while (x < c[1]) {
       fn(g, b[x]);
+      if (g.lane == 0) x = nw + atomicAdd(cl + 1, 1);
+      x = __shfl_sync(0xffffffffu, x, 0);
     }
   }
   {
     TileG<8> g((int)(threadIdx.x & 31));
     const int32_t *b = bl.bin(0);
-    for (;;) {
-      int32_t x = 0;
-      if (g.rank() == 0) x = atomicAdd(cl + 2, 1);
-      x = __shfl_sync(g.mask, x, 0, 8);
-      if (x >= c[0]) break;
+    const int32_t ntl = (gridDim.x * NT) >> 3;
+    int32_t x = (blockIdx.x * NT + threadIdx.x) >> 3;
+    while (x < c[0]) {
       fn(g, b[x]);
+      if (g.rank() == 0) x = ntl + atomicAdd(cl + 2, 1);
+      x = __shfl_sync(g.mask, x, 0, 8);
     }
   }
+}
+
+// Uniform control-word reads (counters published by the last grid barrier): ONE
+// request per CTA, broadcast through shared memory.  If every warp read them, the
+// same L2 line would take ~4.7k requests per word per phase, serialised in one L2
+// slice: ~9 us of floor per phase on B200 (measured with dmf_get_trace_cta).
+// fetch(k) is evaluated by thread k < K.
+template <class F>
+__device__ __forceinline__ void cta_snap(Smem &sm, int K, F fetch) {
+  __syncthreads();
+  if ((int)threadIdx.x < K) sm.cv[threadIdx.x] = fetch((int)threadIdx.x);
+  __syncthreads();
+}
+__device__ __forceinline__ void cta_counts(Smem &sm, const int32_t *p, int32_t c[NB]) {
+  cta_snap(sm, NB, [&](int k) { return (long long)ldv(p + k); });
+#pragma unroll
+  for (int b = 0; b < NB; b++) c[b] = (int32_t)sm.cv[b];
+}
+__device__ __forceinline__ long long cta_ld(Smem &sm, const long long *p) {
+  cta_snap(sm, 1, [&](int) { return ldv(p); });
+  return sm.cv[0];
+}
+__device__ __forceinline__ int32_t cta_ld(Smem &sm, const int32_t *p) {
+  cta_snap(sm, 1, [&](int) { return (long long)ldv(p); });
+  return (int32_t)sm.cv[0];
 }
 
 __device__ __forceinline__ void read_counts(const int32_t *p, int32_t c[NB]) {
@@ -274,10 +320,19 @@ constexpr int TILE_ITEMS = 4;                     // vertices per thread per com
 struct BfsCtx {
   int32_t lvl;
   bool collect;
-  bool bu[2];                       // bottom-up this level, per track
-  bool dense[2];                    // top-down by idempotent stores + compaction, per track
+  uint32_t bu;                      // bit tr: bottom-up this level on track tr
+  uint32_t dense;                   // bit tr: top-down by idempotent stores + compaction
   BL next, wl;
   unsigned long long *fs_next;      // [2] slot counts of the next frontier per track
+  __device__ bool isbu(int tr) const { return (bu >> tr) & 1u; }
+  __device__ bool isdense(int tr) const { return (dense >> tr) & 1u; }
+};
+
+// Per-thread slot sums of the next frontier, per track (two registers: an array
+// indexed by the track would live in local memory).
+struct FS {
+  long long a = 0, b = 0;
+  __device__ void add(int tr, long long x) { if (tr) b += x; else a += x; }
 };
 
 // ---- block-staged appends (Stage is declared with Smem above) ----------------------
@@ -339,8 +394,8 @@ __device__ __forceinline__ int wl_bin(int32_t deg) {
 
 // warp-convergent: claimed vertex -> next frontier (+ worklist if active); counts
 // the claimed vertex's slots into fs[track]
-__device__ __noinline__ void claim_push(const Dev &d, Stage &st, const BfsCtx &c, bool claimed, bool act, int32_t v,
-                                           int tr, long long fs[2]) {
+__device__ __forceinline__ void claim_push(const Dev &d, Stage &st, const BfsCtx &c, bool claimed, bool act, int32_t v,
+                                           int tr, FS &fs) {
   const int32_t deg = claimed ? d.row[v + 1] - d.row[v] : 0;
   const int fb = claimed ? front_bin(deg) : -1;
   const int32_t val = (int32_t)((uint32_t)v | (tr ? TRACK_BIT : 0u));
@@ -361,12 +416,12 @@ __device__ __noinline__ void claim_push(const Dev &d, Stage &st, const BfsCtx &c
 #pragma unroll
     for (int b = 0; b < 4; b++) stage_conv(st, 2 + b, c.wl.bin(b), c.wl.c + b, wb == b, val);
   }
-  if (claimed) fs[tr] += deg;
+  if (claimed) fs.add(tr, deg);
 }
 
 // single-thread version (bottom-up pass B leaders)
 __device__ __forceinline__ void claim_one(const Dev &d, Stage &st, const BfsCtx &c, bool act, int32_t v, int tr,
-                                          long long fs[2]) {
+                                          FS &fs) {
   const int32_t deg = d.row[v + 1] - d.row[v];
   const int32_t val = (int32_t)((uint32_t)v | (tr ? TRACK_BIT : 0u));
   const int fb = front_bin(deg);
@@ -380,7 +435,7 @@ __device__ __forceinline__ void claim_one(const Dev &d, Stage &st, const BfsCtx 
     const int wb = wl_bin(deg);
     stage_one(st, 2 + wb, c.wl.bin(wb), c.wl.c + wb, val);
   }
-  fs[tr] += deg;
+  fs.add(tr, deg);
 }
 
 __device__ __forceinline__ bool activity(const Dev &d, bool collect, int tr, int32_t v) {
@@ -391,11 +446,11 @@ __device__ __forceinline__ bool activity(const Dev &d, bool collect, int tr, int
 
 // one scanned slot (rb = the track's BFS residual, v = head); warp-convergent
 __device__ __forceinline__ void td_slot(const Dev &d, Stage &st, const BfsCtx &c, int tr, int32_t rb, int32_t v,
-                                        long long fs[2]) {
+                                        FS &fs) {
   const Track k = make_track(d, tr);
   bool claimed = false, act = false;
-  const bool ok = rb > 0 && v != k.excl && ldv(k.hgt + v) == d.n;
-  const bool dn = c.dense[tr];          // many discoverers per vertex: a store, deduplicated by compaction
+  const bool ok = rb > 0 && v != k.excl && ldl1(k.hgt + v) == d.n;   // stale n: the CAS decides
+  const bool dn = c.isdense(tr);          // many discoverers per vertex: a store, deduplicated by compaction
   if (dn && ok) k.hgt[v] = c.lvl + 1;
   if (!dn && ok) {
     claimed = atomicCAS(k.hgt + v, d.n, c.lvl + 1) == d.n;
@@ -407,9 +462,9 @@ __device__ __forceinline__ void td_slot(const Dev &d, Stage &st, const BfsCtx &c
 
 // warp per frontier vertex (bin 1): coalesced scan of its row, 4 slots per lane per step
 __device__ __forceinline__ void td_vertex_warp(const Dev &d, Smem &sm, Stage &st, int32_t entry, const BfsCtx &c,
-                                               long long fs[2]) {
+                                               FS &fs) {
   const int tr = ((uint32_t)entry & TRACK_BIT) ? 1 : 0;
-  if (c.bu[tr]) return;
+  if (c.isbu(tr)) return;
   const int lane = threadIdx.x & 31;
   const int32_t w = (int32_t)((uint32_t)entry & ~TRACK_BIT);
   const int32_t beg = d.row[w], end = d.row[w + 1];
@@ -433,10 +488,10 @@ __device__ __forceinline__ void td_vertex_warp(const Dev &d, Smem &sm, Stage &st
 
 // warp per CH-slot chunk of a big frontier row (edge-balanced)
 __device__ __forceinline__ void td_chunk_warp(const Dev &d, Smem &sm, Stage &st, long long ce, const BfsCtx &c,
-                                              long long fs[2]) {
+                                              FS &fs) {
   const uint32_t lo = (uint32_t)ce;
   const int tr = (lo & TRACK_BIT) ? 1 : 0;
-  if (c.bu[tr]) return;
+  if (c.isbu(tr)) return;
   const int lane = threadIdx.x & 31;
   const int32_t w = (int32_t)(lo & ~TRACK_BIT);
   const int32_t rb0 = d.row[w] + (int32_t)(ce >> 32) * CH;
@@ -459,13 +514,13 @@ __device__ __forceinline__ void td_chunk_warp(const Dev &d, Smem &sm, Stage &st,
 // warp over up to 32 low-degree frontier vertices (bin 0): their rows are
 // concatenated and split evenly over the lanes (degree scan + shuffle search)
 __device__ __forceinline__ void td_small_chunk(const Dev &d, Smem &sm, Stage &st, const int32_t *list, int32_t x0,
-                                               int32_t cnt, const BfsCtx &c, long long fs[2]) {
+                                               int32_t cnt, const BfsCtx &c, FS &fs) {
   const int lane = threadIdx.x & 31;
   int32_t entry = 0, beg = 0, deg = 0;
   if (lane < cnt) {
     entry = list[x0 + lane];
     const int32_t w = (int32_t)((uint32_t)entry & ~TRACK_BIT);
-    if (!c.bu[((uint32_t)entry & TRACK_BIT) ? 1 : 0]) {
+    if (!c.isbu(((uint32_t)entry & TRACK_BIT) ? 1 : 0)) {
       beg = d.row[w];
       deg = d.row[w + 1] - beg;
     }
@@ -504,7 +559,7 @@ __device__ __forceinline__ void td_small_chunk(const Dev &d, Smem &sm, Stage &st
 constexpr int32_t BU_THREAD_MAX = 16;
 
 __device__ __forceinline__ void bfs_bottom_up_a(const Dev &d, Smem &sm, Stage &st, const BfsCtx &c, int32_t *bul,
-                                                int32_t *bulc, long long fs[2]) {
+                                                int32_t *bulc, FS &fs) {
   const int32_t n = d.n;
   const int32_t nt = gridDim.x * NT;
   unsigned long long scanned = 0;
@@ -514,8 +569,8 @@ __device__ __forceinline__ void bfs_bottom_up_a(const Dev &d, Smem &sm, Stage &s
     int tr = 0;
     if (v < n) {
       int cand = -1;
-      if (c.bu[0] && v != d.s && ldv(d.hp + v) == n) cand = 0;
-      else if (c.bu[1] && v != d.t && ldv(d.hm + v) == n) cand = 1;
+      if (c.isbu(0) && v != d.s && ldv(d.hp + v) == n) cand = 0;
+      else if (c.isbu(1) && v != d.t && ldv(d.hm + v) == n) cand = 1;
       if (cand >= 0) {
         tr = cand;
         const int32_t beg = d.row[v], end = d.row[v + 1];
@@ -533,7 +588,7 @@ __device__ __forceinline__ void bfs_bottom_up_a(const Dev &d, Smem &sm, Stage &s
             }
 #pragma unroll
             for (int j = 0; j < 4; j++)
-              if (!claimed && r[j] > 0 && ldv(k.hgt + w[j]) == c.lvl) claimed = true;
+              if (!claimed && r[j] > 0 && ldl1(k.hgt + w[j]) == c.lvl) claimed = true;   // level-lvl labels are frozen
             scanned += 4;
           }
           if (claimed) {
@@ -553,7 +608,7 @@ __device__ __forceinline__ void bfs_bottom_up_a(const Dev &d, Smem &sm, Stage &s
 
 template <class G>
 __device__ __forceinline__ void bfs_bottom_up_b(const Dev &d, const G &g, Smem &sm, Stage &st, const BfsCtx &c,
-                                                int32_t entry, long long fs[2]) {
+                                                int32_t entry, FS &fs) {
   const int tr = ((uint32_t)entry & TRACK_BIT) ? 1 : 0;
   const int32_t v = (int32_t)((uint32_t)entry & ~TRACK_BIT);
   const Track k = make_track(d, tr);
@@ -571,7 +626,7 @@ __device__ __forceinline__ void bfs_bottom_up_b(const Dev &d, const G &g, Smem &
     bool hit = false;
 #pragma unroll
     for (int j = 0; j < 4; j++)
-      if (r[j] > 0 && ldv(k.hgt + w[j]) == c.lvl) hit = true;
+      if (r[j] > 0 && ldl1(k.hgt + w[j]) == c.lvl) hit = true;
     scanned += 4 * G::size;
     if (g.any(hit)) { found = true; break; }
   }
@@ -597,7 +652,6 @@ __device__ __forceinline__ void compact_domain(const Dev &d, TileSm &ts, int32_t
   const int lane = threadIdx.x & 31;
   const int32_t tile_sz = TILE_ITEMS * NT;
   WarpG g{lane};
-  int32_t *gcnt[7] = {next.c, next.c + 1, next.c + 3, wl.c, wl.c + 1, wl.c + 2, wl.c + 3};
   for (int32_t t0 = blockIdx.x * tile_sz; t0 < N; t0 += gridDim.x * tile_sz) {
     if (threadIdx.x < 8) ts.cnt[threadIdx.x] = 0;
     __syncthreads();
@@ -661,7 +715,9 @@ __device__ __forceinline__ void compact_domain(const Dev &d, TileSm &ts, int32_t
     __syncthreads();
     if (threadIdx.x < 7) {
       const int32_t cc = ts.cnt[threadIdx.x];
-      ts.base[threadIdx.x] = cc ? atomicAdd(gcnt[threadIdx.x], cc) : 0;
+      const int k = threadIdx.x;     // categories -> global counters
+      int32_t *gc = k == 0 ? next.c : k == 1 ? next.c + 1 : k == 2 ? next.c + 3 : wl.c + (k - 3);
+      ts.base[threadIdx.x] = cc ? atomicAdd(gc, cc) : 0;
     }
     __syncthreads();
 #pragma unroll
@@ -677,10 +733,10 @@ __device__ __forceinline__ void compact_domain(const Dev &d, TileSm &ts, int32_t
 }
 
 // block-wide: flush the stages and publish the per-CTA frontier slot sums
-__device__ __forceinline__ void bfs_flush(Smem &sm, Stage &st, const BfsCtx &c, long long fs[2]) {
+__device__ __forceinline__ void bfs_flush(Smem &sm, Stage &st, const BfsCtx &c, FS &fs) {
   stage_flush(st, c.next, c.wl);
   BlockG bg{sm.red};
-  const long long f0 = bg.sum(fs[0]), f1 = bg.sum(fs[1]);
+  const long long f0 = bg.sum(fs.a), f1 = bg.sum(fs.b);
   if (threadIdx.x == 0) {
     if (f0) atomicAdd(c.fs_next, (unsigned long long)f0);
     if (f1) atomicAdd(c.fs_next + 1, (unsigned long long)f1);
@@ -691,10 +747,10 @@ __device__ __forceinline__ void bfs_flush(Smem &sm, Stage &st, const BfsCtx &c, 
 __device__ __forceinline__ void bfs_expand_level(const Dev &d, cg::grid_group &grid, Smem &sm, Stage &st,
                                                  PhaseClock &clk, int32_t it, const BL &cur, const int32_t c[NB],
                                                  const BfsCtx &ctx, int32_t *bul, int32_t *bulc) {
-  const bool bu = ctx.bu[0] || ctx.bu[1];
-  long long fs[2] = {0, 0};
+  const bool bu = ctx.bu != 0;
+  FS fs;
   if (bu) bfs_bottom_up_a(d, sm, st, ctx, bul, bulc, fs);
-  if (!(ctx.bu[0] && ctx.bu[1])) {
+  if (ctx.bu != 3u) {
     const int32_t gw = blockIdx.x * WPB + (threadIdx.x >> 5), nw = gridDim.x * WPB;
     for (int32_t x = gw; x < c[3]; x += nw) td_chunk_warp(d, sm, st, cur.cq[x], ctx, fs);
     for (int32_t x = gw; x < c[1]; x += nw) td_vertex_warp(d, sm, st, cur.bin(1)[x], ctx, fs);
@@ -702,12 +758,13 @@ __device__ __forceinline__ void bfs_expand_level(const Dev &d, cg::grid_group &g
     for (int32_t x = gw * 32; x < c[0]; x += nw * 32) td_small_chunk(d, sm, st, b0, x, min(32, c[0] - x), ctx, fs);
   }
   bfs_flush(sm, st, ctx, fs);
-  grid.sync();
-  clk.lap(d, sm, ST_T_BFS, it, ctx.lvl, total(c), (ctx.bu[0] ? 1 : 0) | (ctx.bu[1] ? 2 : 0) | (c[3] << 3));
+  gsync(d, grid, sm);
+  clk.lap(d, sm, ST_T_BFS, it, ctx.lvl, total(c), (int32_t)ctx.bu | (c[3] << 3));
   if (bu) {
-    const int32_t q1 = ldv(bulc), q2 = ldv(bulc + 1);
+    cta_snap(sm, 2, [&](int k) { return (long long)ldv(bulc + k); });
+    const int32_t q1 = (int32_t)sm.cv[0], q2 = (int32_t)sm.cv[1];
     if (q1 + q2 > 0) {
-      fs[0] = fs[1] = 0;
+      fs = FS();
       {
         BlockG g{sm.red};
         for (int32_t x = blockIdx.x; x < q2; x += gridDim.x) bfs_bottom_up_b(d, g, sm, st, ctx, bul[d.n + x], fs);
@@ -718,7 +775,7 @@ __device__ __forceinline__ void bfs_expand_level(const Dev &d, cg::grid_group &g
         for (int32_t x = gw; x < q1; x += nw) bfs_bottom_up_b(d, g, sm, st, ctx, bul[x], fs);
       }
       bfs_flush(sm, st, ctx, fs);
-      grid.sync();
+      gsync(d, grid, sm);
       clk.lap(d, sm, ST_T_BFS_BU, it, ctx.lvl, q1 + q2, q2);
     }
   }
@@ -854,7 +911,7 @@ __device__ __forceinline__ void discharge(const Dev &d, const G &g, Smem &sm, in
     }
     if (cyc == d.kc && hu < n && eu > 0) activate(d, k, nxt, u, tag, sm);  // KERNELCYCLES spent
     if (relabelled && d.rlf[u] == 0) { d.rlf[u] = 1; bl_append_one(d, rl, u, tag); }
-    atomicAdd(workc, scanned + 16ull * lifts + 16ull);
+    atomicAdd(&sm.work, scanned + 16ull * lifts + 16ull);
     sstat_add(sm, ST_DIS_V, 1);
     sstat_add(sm, ST_DIS_SLOTS, scanned);
     sstat_add(sm, ST_RELABELS, lifts);
@@ -876,7 +933,7 @@ __device__ __forceinline__ void rie_slots(const Dev &d, const Track &k, int32_t 
     const int32_t r = ldv(k.F + i);
     if (r > 0) {
       const int32_t v = d.dst[i];
-      if (hu > ldv(k.hgt + v) + 1) {
+      if (hu > ldl1(k.hgt + v) + 1) {            // heights are frozen in RIE
         const int32_t ri = d.rev[i];
         k.F[i] = 0;
         k.R[ri] = 0;
@@ -909,7 +966,6 @@ __device__ __forceinline__ void rie(const Dev &d, const G &g, Smem &sm, int32_t 
   moved = g.sum(moved);
   if (g.rank() == 0) {
     if (moved) atom_add(d.e + u, -moved * k.sign);
-    atomicAdd(workc, (unsigned long long)(end - beg));
     sstat_add(sm, ST_RIE_SLOTS, (unsigned long long)(end - beg));
   }
   sstat_add(sm, ST_RIE_SAT, sat);
@@ -938,7 +994,6 @@ __device__ __forceinline__ void rie_chunks(const Dev &d, Smem &sm, const long lo
     moved = g.sum(moved);
     if (lane == 0) {
       if (moved) atom_add(d.e + u, -moved * k.sign);
-      atomicAdd(workc, (unsigned long long)(end - beg));
       sstat_add(sm, ST_RIE_SLOTS, (unsigned long long)(end - beg));
     }
     sstat_add(sm, ST_RIE_SAT, sat);
@@ -949,12 +1004,15 @@ __device__ __forceinline__ void rie_chunks(const Dev &d, Smem &sm, const long lo
 // Roots of a global relabel.
 enum ResetKind : int { RK_PUSH = 0, RK_PP = 1, RK_STAGE2 = 2, RK_MINCUT = 3, RK_MAXCUT = 4, RK_MINCUT_P = 5 };
 
-struct Lists {
-  int32_t *q[2];    // frontier ping-pong, [NB bins][n] each
-  long long *qc[2]; // their chunk queues
-  int32_t *wl[2];   // worklist ping-pong, [NB bins][n] each
-  int32_t *rl;      // relabelled, [NB bins][n]
-  long long *rlc;   // its chunk queue
+struct Lists {      // (members, not arrays: a dynamically indexed array would live in local memory)
+  int32_t *q0, *q1;       // frontier ping-pong, [NB bins][n] each
+  long long *qc0, *qc1;   // their chunk queues
+  int32_t *wl0, *wl1;     // worklist ping-pong, [NB bins][n] each
+  int32_t *rl;            // relabelled, [NB bins][n]
+  long long *rlc;         // its chunk queue
+  __device__ int32_t *q(int i) const { return i ? q1 : q0; }
+  __device__ long long *qc(int i) const { return i ? qc1 : qc0; }
+  __device__ int32_t *wl(int i) const { return i ? wl1 : wl0; }
 };
 
 
@@ -973,7 +1031,9 @@ struct Lists {
 //   mu          accumulated in RESET, read at level 0; zeroed with qc[0]
 // Requires qc[0], fs[0], mu == 0 and wlc == 0 on entry.
 __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseClock &clk, int kind,
-                            const Lists &L, bool collect, bool stage2) {
+                            bool collect, bool stage2) {
+  const size_t nb = (size_t)NB * d.n;
+  const Lists L{d.q0, d.q1, d.cq0, d.cq1, d.wl, d.wl + nb, d.rl, d.cqr};
   const int32_t n = d.n;
   Ctl *ctl = d.ctl;
   int32_t *qc = ctl->qc, *wlc = ctl->wlc, *rlc = ctl->rlc;
@@ -990,12 +1050,13 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
       if (threadIdx.x < 3) ctl->work[threadIdx.x] = 0;
       if (threadIdx.x < 2) { ctl->fs[2 + threadIdx.x] = 0; ctl->bulc[threadIdx.x] = 0; }
     }
-    const int32_t N = on_plist ? ldv(&ctl->pcnt) : n;
+    const int32_t N = on_plist ? cta_ld(sm, &ctl->pcnt) : n;
     {
       // heights: 0 for roots, |V| for the rest of the track's region, |V|+1 outside it
-      long long fs[2] = {0, 0}, mu0 = 0, mu1 = 0;
-      const BfsCtx c0{0, false, {false, false}, {false, false}, BL{L.q[0], qc, n, L.qc[0]},
-                      BL{L.wl[0], wlc, n, nullptr}, ctl->fs};
+      FS fs;
+      long long mu0 = 0, mu1 = 0;
+      const BfsCtx c0{0, false, 0u, 0u, BL{L.q0, qc, n, L.qc0},
+                      BL{L.wl0, wlc, n, nullptr}, ctl->fs};
       for (int32_t b = blockIdx.x * NT + (threadIdx.x & ~31); b < N; b += nt) {
         const int32_t x = b + (threadIdx.x & 31);
         bool r0 = false, r1 = false, in0 = false, in1 = false;
@@ -1045,21 +1106,24 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
       if (lead) sstat_add(sm, ST_RESET_V, (unsigned long long)N);
     }
     beacon(d, 10 + kind, iter, 0, 0);
-    grid.sync();
+    gsync(d, grid, sm);
     clk.lap(d, sm, ST_T_RESET, iter, kind, N);
     // ---------------- BFS levels (fused worklist compaction + termination test)
-    long long mu[2] = {use0 ? ldv(reinterpret_cast<const long long *>(ctl->mu)) : 0,
-                       use1 ? ldv(reinterpret_cast<const long long *>(ctl->mu + 1)) : 0};
+    cta_snap(sm, 2, [&](int k) { return ldv(reinterpret_cast<const long long *>(ctl->mu + k)); });
+    long long mu[2] = {use0 ? sm.cv[0] : 0, use1 ? sm.cv[1] : 0};
     int32_t lvl = 0;
     for (;; ++lvl) {
       int32_t *cur_c = qc + NB * (lvl % 3);
       int32_t c[NB];
-      read_counts(cur_c, c);
+      unsigned long long *fsl = ctl->fs + 2 * (lvl % 3);
+      cta_snap(sm, NB + 2, [&](int k) {
+        return k < NB ? (long long)ldv(cur_c + k) : ldv(reinterpret_cast<const long long *>(fsl + (k - NB)));
+      });
+#pragma unroll
+      for (int b = 0; b < NB; b++) c[b] = (int32_t)sm.cv[b];
+      const long long f0 = sm.cv[NB], f1 = sm.cv[NB + 1];
       beacon(d, 20 + kind, iter, 0, lvl, total(c), c[3]);
       if (total(c) == 0) break;
-      unsigned long long *fsl = ctl->fs + 2 * (lvl % 3);
-      const long long f0 = ldv(reinterpret_cast<const long long *>(fsl));
-      const long long f1 = ldv(reinterpret_cast<const long long *>(fsl + 1));
       if (lvl > 0) { mu[0] -= f0; mu[1] -= f1; }
       if (blockIdx.x == 0 && threadIdx.x < NB) {
         qc[NB * ((lvl + 2) % 3) + threadIdx.x] = 0;
@@ -1072,11 +1136,11 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
       const bool bu1 = f1 > 0 && (unsigned long long)f1 * BU_ALPHA > (unsigned long long)(mu[1] > 0 ? mu[1] : 0);
       const bool dn0 = !bu0 && f0 > 0 && (unsigned long long)f0 * DENSE_DIV >= (unsigned long long)d.S;
       const bool dn1 = !bu1 && f1 > 0 && (unsigned long long)f1 * DENSE_DIV >= (unsigned long long)d.S;
-      const BfsCtx ctx{lvl, collect, {bu0, bu1}, {dn0, dn1},
-                       BL{L.q[(lvl + 1) & 1], qc + NB * ((lvl + 1) % 3), n, L.qc[(lvl + 1) & 1]},
-                       BL{L.wl[0], wlc, n, nullptr}, ctl->fs + 2 * ((lvl + 1) % 3)};
+      const BfsCtx ctx{lvl, collect, (bu0 ? 1u : 0u) | (bu1 ? 2u : 0u), (dn0 ? 1u : 0u) | (dn1 ? 2u : 0u),
+                       BL{L.q((lvl + 1) & 1), qc + NB * ((lvl + 1) % 3), n, L.qc((lvl + 1) & 1)},
+                       BL{L.wl0, wlc, n, nullptr}, ctl->fs + 2 * ((lvl + 1) % 3)};
       if (lead && (bu0 || bu1)) sstat_add(sm, ST_BU_LEVELS, 1);
-      bfs_expand_level(d, grid, sm, sm.st, clk, iter, BL{L.q[lvl & 1], cur_c, n, L.qc[lvl & 1]}, c, ctx, d.bul,
+      bfs_expand_level(d, grid, sm, sm.st, clk, iter, BL{L.q(lvl & 1), cur_c, n, L.qc(lvl & 1)}, c, ctx, d.bul,
                        ctl->bulc + 2 * (lvl & 1));
       if (dn0 || dn1) {                             // dense top-down tracks: build lvl+1 by compaction
         long long g0 = 0, g1 = 0;
@@ -1092,14 +1156,14 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
           if (g0) atomicAdd(ctx.fs_next, (unsigned long long)g0);
           if (g1) atomicAdd(ctx.fs_next + 1, (unsigned long long)g1);
         }
-        grid.sync();
+        gsync(d, grid, sm);
         clk.lap(d, sm, ST_T_BFS_CMP, iter, lvl, N);
       }
     }
     if (lead) sstat_add(sm, ST_LEVELS, (unsigned long long)lvl);
     {
       int32_t w0[NB];
-      read_counts(wlc, w0);
+      cta_counts(sm, wlc, w0);
       if (total(w0) == 0) break;                  // no active vertex: converged (R9)
     }
     if (lead) {
@@ -1119,26 +1183,31 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
       // only when every block has passed the barrier after its last read
       const int cur = r % 3, nx = (r + 1) % 3, nn = (r + 2) % 3;
       int32_t w[NB];
-      read_counts(wlc + NB * cur, w);
+      cta_counts(sm, wlc + NB * cur, w);
       beacon(d, 30 + kind, iter, r, 0, total(w), w[3]);
       if (blockIdx.x == 0 && threadIdx.x < NB) {
         wlc[NB * nn + threadIdx.x] = 0;           // last read in round r-1 (before its barrier)
         if (threadIdx.x < 3) ctl->claim[3 * nn + threadIdx.x] = 0;   // claimed in round r-1
         if (threadIdx.x == 0) ctl->work[nx] = 0;  // last read at the end of round r-2; filled in round r+1
       }
-      const BL nxt{L.wl[(r + 1) & 1], wlc + NB * nx, n, nullptr};
-      process_bl_dyn(BL{L.wl[r & 1], wlc + NB * cur, n, nullptr}, w, sm, ctl->claim + 3 * cur,
+      const BL nxt{L.wl((r + 1) & 1), wlc + NB * nx, n, nullptr};
+      process_bl_dyn(BL{L.wl(r & 1), wlc + NB * cur, n, nullptr}, w, sm, ctl->claim + 3 * cur,
                      [&](auto &g, int32_t entry) { discharge(d, g, sm, entry, rl, nxt, ctl->work + cur); });
+      __syncthreads();
+      if (threadIdx.x == 0 && sm.work) { atomicAdd(ctl->work + cur, sm.work); sm.work = 0; }
       if (lead) sstat_add(sm, ST_ROUNDS, 1);
-      grid.sync();
+      gsync(d, grid, sm);
       clk.lap(d, sm, ST_T_DIS, iter, r, total(w), w[3]);
       int32_t wn[NB];
-      read_counts(wlc + NB * nx, wn);
+      cta_snap(sm, NB + 1, [&](int k) {
+        return k < NB ? (long long)ldv(wlc + NB * nx + k) : ldv(reinterpret_cast<const long long *>(ctl->work + cur));
+      });
+#pragma unroll
+      for (int b = 0; b < NB; b++) wn[b] = (int32_t)sm.cv[b];
       // a round's barrier + latency floor is charged like S/16 scanned slots, so that
       // long tails of near-empty rounds (excess creeping up one lift at a time) hand
       // over to a global relabel, which lifts unreachable vertices to |V| at once
-      spent += (unsigned long long)ldv(reinterpret_cast<const long long *>(ctl->work + cur)) +
-               (unsigned long long)(d.S >> 4);
+      spent += (unsigned long long)sm.cv[NB] + (unsigned long long)(d.S >> 4);
       if (total(wn) == 0) break;
       if (r + 1 >= MAX_ROUNDS || (long long)spent > d.work_budget) {   // hand the rest to a global relabel
         if (lead) sstat_add(sm, ST_BUDGET_STOPS, 1);
@@ -1159,12 +1228,12 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
     }
     {
       int32_t rc[NB];
-      read_counts(rlc, rc);
+      cta_counts(sm, rlc, rc);
       beacon(d, 40 + kind, iter, 0, 0, total(rc), rc[3]);
       rie_chunks(d, sm, rl.cq, rc[3], rl, ctl->work);
       const int32_t rc2[NB] = {rc[0], rc[1], 0, 0};
       process_bl(rl, rc2, sm, [&](auto &g, int32_t entry) { rie(d, g, sm, entry, rl, ctl->work); });
-      grid.sync();
+      gsync(d, grid, sm);
       clk.lap(d, sm, ST_T_RIE, iter, 0, total(rc), rc[3]);
     }
   }
@@ -1199,26 +1268,25 @@ __device__ __forceinline__ long long saturate_slot(const Dev &d, int32_t i) {
 }
 
 template <int NTHREADS>
-__global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(Dev d, int32_t mode) {
+__global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(const __grid_constant__ Dev d, int32_t mode) {
   cg::grid_group grid = cg::this_grid();
   __shared__ Smem sm;
   for (int i = threadIdx.x; i < ST_N; i += NTHREADS) sm.stat[i] = 0;
   if (threadIdx.x < 6) sm.st.cnt[threadIdx.x] = 0;
+  if (threadIdx.x == 0) { sm.work = 0; sm.tprev = gtimer(); }
   __syncthreads();
   const int32_t n = d.n;
   const int32_t gt = blockIdx.x * NTHREADS + threadIdx.x, nt = gridDim.x * NTHREADS;
   Ctl *ctl = d.ctl;
-  const size_t nb = (size_t)NB * n;
-  const Lists L{{d.q0, d.q1}, {d.cq0, d.cq1}, {d.wl, d.wl + nb}, d.rl, d.cqr};
   BlockG bg{sm.red};
   PhaseClock clk;
-  clk.start();
+  clk.start(sm);
 
   if (mode == MODE_STATIC) {
     // Alg.1 l.1-8: e = 0, c_f = c  (and the mirror)
     for (int64_t i = gt; i < d.S; i += nt) { d.res[i] = d.cap[i]; d.rres[i] = d.cap[d.rev[i]]; }
     for (int32_t v = gt; v < n; v += nt) d.e[v] = 0;
-    grid.sync();
+    gsync(d, grid, sm);
   } else if (mode == MODE_PR || mode == MODE_PP) {
     // ---- Updates Processing (Alg.5), validated first (R11)
     for (int64_t j = gt; j < d.k; j += nt) {
@@ -1230,8 +1298,9 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(Dev d, int32_t m
       else if (atomicExch(d.stamp + slot, d.batch_id) == d.batch_id) set_status(d, -3, (int32_t)j);
       d.bslot[j] = slot;
     }
-    grid.sync();
-    if (ldv(&ctl->status) != 0) mode = -1;       // all-or-nothing: state untouched
+    gsync(d, grid, sm);
+    clk.lap(d, sm, ST_T_PRO, 0, 1, (int32_t)d.k);
+    if (cta_ld(sm, &ctl->status) != 0) mode = -1;   // all-or-nothing: state untouched
     // Alg.5 l.1-3 (c_f += c' - c) and l.4-11 (a negative slot returns its excess flow:
     // e(u) += d, e(v) -= d, R10) fused per entry: the clamp of slot i depends only on
     // c_f(i) + delta_i (the entry of the reverse slot never changes c_f(i) unless it
@@ -1266,7 +1335,10 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(Dev d, int32_t m
         atom_add(d.e + u, -(long long)r);
       }
     }
-    if (mode >= 0) grid.sync();
+    if (mode >= 0) {
+      gsync(d, grid, sm);
+      clk.lap(d, sm, ST_T_PRO, 0, 2, (int32_t)d.k);
+    }
   }
   if (mode == MODE_STATIC || mode == MODE_PR) {
     // Alg.1 l.9-13 / Alg.4 l.3-8 (R3): saturate every residual out-slot of s
@@ -1275,9 +1347,9 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(Dev d, int32_t m
     for (int32_t i = beg + gt; i < end; i += nt) tot += saturate_slot(d, i);
     tot = bg.sum(tot);
     if (threadIdx.x == 0 && tot) atom_add(d.e + d.s, -tot);
-    grid.sync();
+    gsync(d, grid, sm);
     clk.lap(d, sm, ST_T_PRO);
-    device_loop(d, grid, sm, clk, RK_PUSH, L, true, false);
+    device_loop(d, grid, sm, clk, RK_PUSH, true, false);
     // part from the final fresh BFS (S = unreached = S_max, R15) + flow (R8)
     long long f = 0;
     for (int32_t v = gt; v < n; v += nt) {
@@ -1290,7 +1362,7 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(Dev d, int32_t m
   } else if (mode == MODE_PP) {
     // ---- stage 1: push on T || pull on S (Alg.8 l.15-28)
     clk.lap(d, sm, ST_T_PRO);
-    device_loop(d, grid, sm, clk, RK_PP, L, true, false);
+    device_loop(d, grid, sm, clk, RK_PP, true, false);
     // ---- P = {h+ = |V| and h- = |V|} (Alg.8 l.29-33), vertices with slots only
     if (blockIdx.x == 0 && threadIdx.x < NB) {
       ctl->qc[threadIdx.x] = 0;
@@ -1305,13 +1377,13 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(Dev d, int32_t m
       }
       warp_append(inP, v, d.plist, &ctl->pcnt);
     }
-    grid.sync();
-    if (threadIdx.x == 0 && blockIdx.x == 0) sstat_add(sm, ST_S2_V, (unsigned long long)ldv(&ctl->pcnt));
+    gsync(d, grid, sm);
+    const int32_t pc = cta_ld(sm, &ctl->pcnt);
+    if (threadIdx.x == 0 && blockIdx.x == 0) sstat_add(sm, ST_S2_V, (unsigned long long)pc);
     // ---- stage 2: Dynamic Push-Relabel restricted to P (Alg.8 l.34)
     clk.lap(d, sm, ST_T_EPI);
-    const int32_t pc = ldv(&ctl->pcnt);
     if (pc > 0) {
-      device_loop(d, grid, sm, clk, RK_STAGE2, L, true, true);
+      device_loop(d, grid, sm, clk, RK_STAGE2, true, true);
       // ---- S_min (R19) = stage 1's final forward reach from {s} u Exc_S (h- < |V|)
       //      united with the forward reach, inside P, of the excess left in P: no
       //      residual edge enters P from S\P or leaves P towards T\P
@@ -1319,8 +1391,8 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(Dev d, int32_t m
         ctl->qc[threadIdx.x] = 0;
         if (threadIdx.x < 2) { ctl->fs[threadIdx.x] = 0; ctl->mu[threadIdx.x] = 0; }
       }
-      grid.sync();
-      device_loop(d, grid, sm, clk, RK_MINCUT_P, L, false, false);
+      gsync(d, grid, sm);
+      device_loop(d, grid, sm, clk, RK_MINCUT_P, false, false);
     }
     // ---- relabel partitions (Alg.8 l.35-49) and F (= sum over T' of e, R8)
     for (int32_t x = gt; x < pc; x += nt) {
@@ -1336,7 +1408,7 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(Dev d, int32_t m
     f = bg.sum(f);
     if (threadIdx.x == 0 && f) atomicAdd(reinterpret_cast<unsigned long long *>(&ctl->flow), (unsigned long long)f);
   } else if (mode == MODE_MINCUT || mode == MODE_MAXCUT) {
-    device_loop(d, grid, sm, clk, mode == MODE_MINCUT ? RK_MINCUT : RK_MAXCUT, L, false, false);
+    device_loop(d, grid, sm, clk, mode == MODE_MINCUT ? RK_MINCUT : RK_MAXCUT, false, false);
     for (int32_t v = gt; v < n; v += nt)
       d.mask[v] = mode == MODE_MINCUT ? (ldv(d.hm + v) < n ? 1 : 0) : (ldv(d.hp + v) < n ? 0 : 1);
   }

@@ -1,6 +1,7 @@
 """Print the per-phase trace of a PP batch / PR batch / static solve on RMAT-20."""
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
 import workloads as W
 import paper_2511_05895_b200 as P
 
@@ -11,10 +12,15 @@ f.set_trace(8192)
 def show(tag):
     st = f.stats()
     print(f"== {tag}: {st['device_ms']:.3f} ms")
-    for r in f.trace():
+    cta = f.trace_cta()
+    for ri, r in enumerate(f.trace()):
         ex = r['extra']
         extra = f"bu={ex & 3} sp={(ex >> 2) & 1} ch={ex >> 3}" if r['phase'] == 'bfs' else f"x={ex}"
-        print(f"  {r['phase']:9s} it={r['iter']:<3d} sub={r['sub']:<4d} items={r['items']:<9d} {extra:16s} {r['us']:9.1f} us")
+        if r['phase'] == 'discharge':
+            extra += f" slow={r['slow_us']:.1f}us deg={r['slow_deg']} cyc={r['slow_cyc']}"
+        c = np.sort(cta[ri]) if ri < len(cta) else np.zeros(1)
+        dist = f"cta busy p50={c[len(c) // 2]:.1f} p90={c[int(len(c) * .9)]:.1f} max={c[-1]:.1f}"
+        print(f"  {r['phase']:9s} it={r['iter']:<3d} sub={r['sub']:<4d} items={r['items']:<9d} {extra:16s} {r['us']:9.1f} us  {dist}")
 f.static_solve(); show("static")
 cs = W.CapState(g)
 for j, algo in enumerate(["pp", "pp", "pr"]):
