@@ -81,6 +81,8 @@ struct dmf_graph {
   int32_t batch_id = 0;
   bool solved = false;
   bool smin_valid = false;   // g->mask holds S_min of the current state
+  bool warm = false;         // hp/hm/part hold the final labels of the last DYN_PP repair
+  bool no_warm = false;      // DMF_NO_WARM=1: always run stage 1's initial global relabel
   int64_t launches = 0;      // kernels launched by solve / apply / cut calls since create
   int64_t flow = 0;
   dmf_stats stats{};
@@ -212,6 +214,7 @@ static Dev make_dev(dmf_graph *g) {
   d.n = g->n; d.s = g->s; d.t = g->t; d.kc = g->kc;
   d.max_iters = g->opt.max_iters > 0 ? g->opt.max_iters : (int32_t)(4LL * g->n + 64 > 0x3fffffff ? 0x3fffffff : 4LL * g->n + 64);
   d.batch_id = g->batch_id;
+  d.warm = g->warm ? 1 : 0;
   d.work_budget = g->S + 6LL * g->n;     // ~ the cost of one whole-graph global relabel
   d.S = g->S; d.k = 0;
   d.row = g->row; d.dst = g->dst; d.rev = g->rev; d.cap = g->cap; d.res = g->res; d.rres = g->rres;
@@ -231,6 +234,8 @@ static Dev make_dev(dmf_graph *g) {
 static int run_solve(dmf_graph *g, int32_t mode, const Dev &dv) {
   Dev d = dv;
   if (mode != MODE_MINCUT) g->smin_valid = false;  // the state (or the mask buffer) is about to change
+  const bool warm_before = g->warm;
+  g->warm = false;                                  // every launch rewrites hp or hm
   CK(cudaMemsetAsync(g->ctl, 0, sizeof(Ctl), g->stream));
   CK(cudaEventRecord(g->ev0, g->stream));
   int32_t md = mode;
@@ -291,6 +296,7 @@ static int run_solve(dmf_graph *g, int32_t mode, const Dev &dv) {
                      : c.status == DMF_EINVAL ? "vertex id out of range"
                      : c.status == DMF_EOVERFLOW ? "capacity outside [0, DMF_CAP_MAX]"
                      : c.status == DMF_ENOCONV ? "iteration cap reached" : "error";
+    if (c.status != DMF_ENOCONV) g->warm = warm_before;   // rejected before any mutation
     return fail(c.status, "%s (batch entry %d)", what, c.err_entry);
   }
   if (mode == MODE_STATIC || mode == MODE_PR || mode == MODE_PP) {
@@ -298,6 +304,7 @@ static int run_solve(dmf_graph *g, int32_t mode, const Dev &dv) {
     g->solved = true;
   }
   g->smin_valid = mode == MODE_PP || mode == MODE_MINCUT;   // MAXCUT / STATIC / PR leave no S_min
+  g->warm = mode == MODE_PP && !g->no_warm;
   return DMF_OK;
 }
 
@@ -431,6 +438,7 @@ int dmf_create(int32_t n, const int64_t *row_ptr, const int32_t *col, const int3
     return bail(DMF_ENOMEM);
   }
   CKB(cudaMallocHost((void **)&g->hctl, sizeof(Ctl)));
+  if (const char *nw = getenv("DMF_NO_WARM")) g->no_warm = atoi(nw) != 0;
   if (const char *wd = getenv("DMF_WATCHDOG_S")) {
     g->watchdog_s = atof(wd);
     CKB(cudaHostAlloc((void **)&g->hdbg, 64, cudaHostAllocMapped));

@@ -76,6 +76,7 @@ struct Ctl {
 struct Dev {
   int32_t n, s, t, kc, max_iters;
   int32_t batch_id;
+  int32_t warm;              // MODE_PP: hp/hm/part are the previous DYN_PP call's final labels (warm start)
   long long work_budget;     // discharge work (slots scanned) allowed between two global relabels
   int64_t S, k;
   const int32_t *__restrict__ row;

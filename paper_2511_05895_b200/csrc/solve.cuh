@@ -1031,7 +1031,7 @@ struct Lists {      // (members, not arrays: a dynamically indexed array would l
 //   mu          accumulated in RESET, read at level 0; zeroed with qc[0]
 // Requires qc[0], fs[0], mu == 0 and wlc == 0 on entry.
 __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseClock &clk, int kind,
-                            bool collect, bool stage2) {
+                            bool collect, bool stage2, bool warm = false) {
   const size_t nb = (size_t)NB * d.n;
   const Lists L{d.q0, d.q1, d.cq0, d.cq1, d.wl, d.wl + nb, d.rl, d.cqr};
   const int32_t n = d.n;
@@ -1043,6 +1043,10 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
   const bool on_plist = kind == RK_STAGE2 || kind == RK_MINCUT_P;
   const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
   for (int iter = 0;; ++iter) {
+   // warm start (DYN_PP after DYN_PP): iteration 0 discharges the worklist seeded by
+   // the batch prologue on the previous call's final labels; the fresh BFS of
+   // iteration 1 still decides termination (R9), so stale labels cost work only
+   if (!(warm && iter == 0)) {
     // ---------------- RESET: heights of the domain, roots -> frontier level 0
     if (blockIdx.x == 0 && threadIdx.x < NB) {
       rlc[threadIdx.x] = 0;
@@ -1166,6 +1170,7 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
       cta_counts(sm, wlc, w0);
       if (total(w0) == 0) break;                  // no active vertex: converged (R9)
     }
+   }
     if (lead) {
       sstat_add(sm, ST_ITERS, 1);
       if (stage2) sstat_add(sm, ST_S2_ITERS, 1);
@@ -1339,6 +1344,33 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(const __grid_con
       gsync(d, grid, sm);
       clk.lap(d, sm, ST_T_PRO, 0, 2, (int32_t)d.k);
     }
+    if (mode == MODE_PP && d.warm) {
+      // Warm start of Alg.8 stage 1: only batch endpoints changed excess, so the
+      // new roots (T-deficits for h+, S-excess for h-, Alg.8 l.16-24) drop to 0 and
+      // the active ones seed round 0's worklist (ring slot 0, deduplicated by inq)
+      const BL wl0{d.wl, ctl->wlc, n, nullptr};
+      for (int64_t j = gt; j < 2 * d.k; j += nt) {
+        const int32_t x = (j & 1) ? d.bv[j >> 1] : d.bu[j >> 1];
+        if (x == d.s || x == d.t) continue;
+        const uint8_t p = ldv(d.part + x);
+        const long long ev = ldv(d.e + x);
+        if (p == PART_T) {
+          if (ev < 0) d.hp[x] = 0;
+          else if (ev > 0 && ldv(d.hp + x) < n && atomicCAS(d.inq + x, 0, 1) == 0) {
+            bl_append_one(d, wl0, x, 0u);
+            sstat_add(sm, ST_ACTIVATIONS, 1);
+          }
+        } else if (p == PART_S) {
+          if (ev > 0) d.hm[x] = 0;
+          else if (ev < 0 && ldv(d.hm + x) < n && atomicCAS(d.inq + x, 0, 1) == 0) {
+            bl_append_one(d, wl0, x, TRACK_BIT);
+            sstat_add(sm, ST_ACTIVATIONS, 1);
+          }
+        }
+      }
+      gsync(d, grid, sm);
+      clk.lap(d, sm, ST_T_PRO, 0, 3, (int32_t)d.k);
+    }
   }
   if (mode == MODE_STATIC || mode == MODE_PR) {
     // Alg.1 l.9-13 / Alg.4 l.3-8 (R3): saturate every residual out-slot of s
@@ -1362,7 +1394,7 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(const __grid_con
   } else if (mode == MODE_PP) {
     // ---- stage 1: push on T || pull on S (Alg.8 l.15-28)
     clk.lap(d, sm, ST_T_PRO);
-    device_loop(d, grid, sm, clk, RK_PP, true, false);
+    device_loop(d, grid, sm, clk, RK_PP, true, false, d.warm != 0);
     // ---- P = {h+ = |V| and h- = |V|} (Alg.8 l.29-33), vertices with slots only
     if (blockIdx.x == 0 && threadIdx.x < NB) {
       ctl->qc[threadIdx.x] = 0;
@@ -1395,9 +1427,11 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(const __grid_con
       device_loop(d, grid, sm, clk, RK_MINCUT_P, false, false);
     }
     // ---- relabel partitions (Alg.8 l.35-49) and F (= sum over T' of e, R8)
-    for (int32_t x = gt; x < pc; x += nt) {
-      const int32_t v = d.plist[x];
-      d.part[v] = ldv(d.hp + v) < n ? PART_T : PART_S;
+    for (int32_t x = gt; x < pc; x += nt) {     // (+ the region encoding of the next warm start:
+      const int32_t v = d.plist[x];              //  h+ = |V|+1 on S', h- = |V|+1 on T')
+      const bool tside = ldv(d.hp + v) < n;
+      d.part[v] = tside ? PART_T : PART_S;
+      if (tside) d.hm[v] = n + 1; else d.hp[v] = n + 1;
     }
     long long f = 0;
     for (int32_t v = gt; v < n; v += nt) {
