@@ -64,7 +64,8 @@ struct dmf_graph {
   int32_t *row = nullptr, *dst = nullptr, *rev = nullptr, *cap = nullptr, *res = nullptr, *rres = nullptr;
   int32_t *hp = nullptr, *hm = nullptr, *q0 = nullptr, *q1 = nullptr, *wl = nullptr, *rl = nullptr;
   int32_t *plist = nullptr, *stamp = nullptr, *inq = nullptr, *bul = nullptr;
-  long long *cq0 = nullptr, *cq1 = nullptr, *cqr = nullptr;
+  long long *cq0 = nullptr, *cq1 = nullptr, *cqr = nullptr, *cw0 = nullptr, *cw1 = nullptr;
+  int32_t *dcnt = nullptr, *dmin = nullptr;
   long long *e = nullptr;
   uint8_t *part = nullptr, *mask = nullptr, *rlf = nullptr;
   int32_t *bbuf = nullptr;   // batch staging: u, v, c, slot  (4 * bcap)
@@ -221,7 +222,8 @@ static Dev make_dev(dmf_graph *g) {
   d.e = g->e; d.hp = g->hp; d.hm = g->hm; d.part = g->part;
   d.q0 = g->q0; d.q1 = g->q1;
   d.wl = g->wl; d.rl = g->rl; d.inq = g->inq; d.bul = g->bul; d.rlf = g->rlf;
-  d.cq0 = g->cq0; d.cq1 = g->cq1; d.cqr = g->cqr;
+  d.cq0 = g->cq0; d.cq1 = g->cq1; d.cqr = g->cqr; d.cw0 = g->cw0; d.cw1 = g->cw1;
+  d.dcnt = g->dcnt; d.dmin = g->dmin;
   d.plist = g->plist; d.stamp = g->stamp;
   d.mask = g->mask; d.ctl = g->ctl;
   d.dbg = g->ddbg;
@@ -429,11 +431,16 @@ int dmf_create(int32_t n, const int64_t *row_ptr, const int32_t *col, const int3
   g->cq0 = (long long *)g->alloc(cqn * 8);
   g->cq1 = (long long *)g->alloc(cqn * 8);
   g->cqr = (long long *)g->alloc(cqn * 8);
+  g->cw0 = (long long *)g->alloc(cqn * 8);
+  g->cw1 = (long long *)g->alloc(cqn * 8);
+  g->dcnt = (int32_t *)g->alloc(nn * 4);
+  g->dmin = (int32_t *)g->alloc(nn * 4);
   g->rl = (int32_t *)g->alloc(NB * nn * 4);
   g->plist = (int32_t *)g->alloc(nn * 4);
   g->ctl = (Ctl *)g->alloc(sizeof(Ctl));
   if (!g->row || !g->dst || !g->rev || !g->cap || !g->res || !g->rres || !g->stamp || !g->e || !g->hp || !g->hm ||
-      !g->part || !g->mask || !g->q0 || !g->q1 || !g->wl || !g->rl || !g->plist || !g->ctl || !g->inq || !g->rlf || !g->bul || !g->cq0 || !g->cq1 || !g->cqr) {
+      !g->part || !g->mask || !g->q0 || !g->q1 || !g->wl || !g->rl || !g->plist || !g->ctl || !g->inq || !g->rlf || !g->bul || !g->cq0 || !g->cq1 || !g->cqr ||
+      !g->cw0 || !g->cw1 || !g->dcnt || !g->dmin) {
     fail(DMF_ENOMEM, "device allocation failed (state, S=%lld)", (long long)S);
     return bail(DMF_ENOMEM);
   }
@@ -447,6 +454,8 @@ int dmf_create(int32_t n, const int64_t *row_ptr, const int32_t *col, const int3
   }
   CKB(cudaMemsetAsync(g->inq, 0, nn * 4, st));
   CKB(cudaMemsetAsync(g->rlf, 0, nn, st));
+  CKB(cudaMemsetAsync(g->dcnt, 0, nn * 4, st));
+  CKB(cudaMemsetAsync(g->dmin, 0x7f, nn * 4, st));   // DMIN_NONE
   if (S) {
     CKB(cudaMemsetAsync(err, 0, 64, st));
     k_rows<<<blocks(nn + 1), TB, 0, st>>>(n, S, ukey, g->row);

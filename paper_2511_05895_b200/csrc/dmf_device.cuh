@@ -27,6 +27,9 @@ constexpr int32_t BIN2_MAX = 8192;
 // Entries of queues / worklists carry the track in bit 31 (vertex ids < 2^31).
 constexpr uint32_t TRACK_BIT = 0x80000000u;
 
+// dmin sentinel (memset byte 0x7f): above every height (heights are <= |V|+1 < 2^31-1)
+constexpr int32_t DMIN_NONE = 0x7f7f7f7f;
+
 // Partition labels of Alg.8.  S'/T' are stored as S/T.
 enum : uint8_t { PART_NONE = 0, PART_S = 1, PART_T = 2, PART_P = 3 };
 
@@ -93,6 +96,9 @@ struct Dev {
   uint8_t *rlf;              // per-vertex "already in the relabelled list" flag
   int32_t *bul;              // bottom-up candidate queue [2 bins][n]
   long long *cq0, *cq1, *cqr; // chunk queues of the frontier ping-pong and of the relabelled list
+  long long *cw0, *cw1;      // chunk queues of the discharge worklist ping-pong (vertices of > BIN1_MAX slots)
+  int32_t *dcnt;             // chunked discharge: chunks of u finished in the current round
+  int32_t *dmin;             // chunked discharge: lowest height among u's slots left residual (DMIN_NONE if none)
   int32_t *plist;            // region P of push-pull stage 2
   int32_t *stamp;            // per-slot batch stamp (duplicate detection)
   const int32_t *bu, *bv, *bc;  // batch entries

@@ -61,6 +61,9 @@ struct Smem {
   unsigned long long tprev;        // trace mode: this CTA's last barrier exit
   unsigned long long tclk;         // PhaseClock: block 0's last lap
   long long cv[8];                 // control words snapped once per CTA (cta_snap)
+  int32_t acnt, rcnt;              // discharge: staged activations / relabelled vertices (in st.f / st.w)
+  int32_t ccnt;                    // discharge: staged push heads (activation candidates)
+  int32_t cand[2048];
   Stage st;                    // block-staged appends (BFS)
   TileSm ts;                   // tiled compaction (dense top-down BFS levels)
 };
@@ -289,12 +292,55 @@ __device__ __forceinline__ int32_t total(const int32_t c[NB]) {
 
 // Queue a vertex whose excess (track-signed) just crossed from <= 0 to > 0 for the
 // next discharge round, at most once per round (inq flag).
+// Discharge-phase appends are BLOCK-STAGED: the entry goes to a shared-memory list
+// (activations in st.f, relabelled vertices in st.w) and vflush moves each CTA's list
+// to the global binned list with one global atomic per bin at the end of the round
+// (a single global counter per list took one L2 atomic per activation, serialised
+// in one L2 slice).  Overflow goes straight to the global list.
+constexpr int32_t ACAP = 2 * SF;     // staged activations per CTA
+constexpr int32_t RCAP = 4 * SW;     // staged relabelled vertices per CTA
+__device__ __forceinline__ int32_t *act_buf(Smem &sm);
+__device__ __forceinline__ int32_t *rel_buf(Smem &sm);
+
 __device__ __forceinline__ void activate(const Dev &d, const Track &k, const BL &nxt, int32_t v, uint32_t tag,
                                          Smem &sm) {
   if (v == d.s || v == d.t) return;
   if (atomicCAS(d.inq + v, 0, 1) != 0) return;     // (a vertex at height >= |V| exits at once)
-  bl_append_one(d, nxt, v, tag);
+  const int32_t pos = atomicAdd(&sm.acnt, 1);
+  if (pos < ACAP) act_buf(sm)[pos] = (int32_t)((uint32_t)v | tag);
+  else bl_append_one(d, nxt, v, tag);
   sstat_add(sm, ST_ACTIVATIONS, 1);
+}
+// One push of d on slot i = (u,v) of track k (ri = rev[i]): the four residual updates and
+// e(v) += d are fire-and-forget reductions; v is staged as an activation CANDIDATE that
+// dis_flush checks once per round (e(v) > 0 after a fence: the last pusher into v sees
+// every push), so no push waits for an atomic's return.  Candidate overflow falls back
+// to the returning atomic and the 0-crossing test.
+constexpr int32_t CCAP = 2048;
+__device__ __forceinline__ void push_slot(const Dev &d, const Track &k, const BL &nxt, int32_t i, int32_t ri, int32_t v,
+                                          int32_t take, uint32_t tag, Smem &sm);
+
+__device__ __forceinline__ void stage_relabelled(const Dev &d, const BL &rl, int32_t u, uint32_t tag, Smem &sm) {
+  const int32_t pos = atomicAdd(&sm.rcnt, 1);
+  if (pos < RCAP) rel_buf(sm)[pos] = (int32_t)((uint32_t)u | tag);
+  else bl_append_one(d, rl, u, tag);
+}
+
+__device__ __forceinline__ void push_slot(const Dev &d, const Track &k, const BL &nxt, int32_t i, int32_t ri, int32_t v,
+                                          int32_t take, uint32_t tag, Smem &sm) {
+  atomicSub(k.F + i, take);          // c_f(u,v) -= d
+  atomicSub(k.R + ri, take);         //   mirror
+  atomicAdd(k.F + ri, take);         // c_f(v,u) += d
+  atomicAdd(k.R + i, take);          //   mirror
+  const int32_t pos = atomicAdd(&sm.ccnt, 1);
+  if (pos < CCAP) {
+    atom_add(d.e + v, (long long)take * k.sign);                           // e(v) += d
+    sm.cand[pos] = (int32_t)((uint32_t)v | tag);
+  } else {
+    const long long eo = (long long)atomicAdd(reinterpret_cast<unsigned long long *>(d.e + v),
+                                              (unsigned long long)((long long)take * k.sign)) * k.sign;
+    if (eo <= 0 && eo + take > 0) activate(d, k, nxt, v, tag, sm);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -392,6 +438,20 @@ __device__ __forceinline__ int wl_bin(int32_t deg) {
   return deg <= BIN0_MAX ? 0 : (deg <= BIN1_MAX ? 1 : (deg <= BIN2_MAX ? 2 : 3));
 }
 
+// warp-convergent: every lane with pred appends ceil(deg/CH) chunk entries of v to bl's
+// chunk queue (count in bl.c[3]); one global atomic per warp
+__device__ __forceinline__ void chunks_conv(const BL &bl, bool pred, int32_t deg, int32_t v, uint32_t tag) {
+  if (__ballot_sync(0xffffffffu, pred) == 0) return;
+  const int32_t nch = pred ? (deg + CH - 1) / CH : 0;
+  WarpG g{(int)(threadIdx.x & 31)};
+  long long tot;
+  const int32_t ex = (int32_t)g.exscan(nch, tot);
+  int32_t base = 0;
+  if (g.lane == 0) base = atomicAdd(bl.c + 3, (int32_t)tot);
+  base = __shfl_sync(0xffffffffu, base, 0);
+  for (int32_t k = 0; k < nch; k++) bl.cq[base + ex + k] = chunk_entry(v, tag, k);
+}
+
 // warp-convergent: claimed vertex -> next frontier (+ worklist if active); counts
 // the claimed vertex's slots into fs[track]
 __device__ __forceinline__ void claim_push(const Dev &d, Stage &st, const BfsCtx &c, bool claimed, bool act, int32_t v,
@@ -411,10 +471,12 @@ __device__ __forceinline__ void claim_push(const Dev &d, Stage &st, const BfsCtx
     base = __shfl_sync(0xffffffffu, base, 0);
     for (int32_t k = 0; k < nch; k++) c.next.cq[base + ex + k] = chunk_entry(v, tr ? TRACK_BIT : 0u, k);
   }
-  if (c.collect) {
+  if (c.collect) {                  // active: queued for discharge round 0 (inq: see activate)
     const int wb = act ? wl_bin(deg) : -1;
-#pragma unroll
-    for (int b = 0; b < 4; b++) stage_conv(st, 2 + b, c.wl.bin(b), c.wl.c + b, wb == b, val);
+    if (act) d.inq[v] = 1;
+    stage_conv(st, 2, c.wl.bin(0), c.wl.c, wb == 0, val);
+    stage_conv(st, 3, c.wl.bin(1), c.wl.c + 1, wb == 1, val);
+    chunks_conv(c.wl, wb >= 2, deg, v, tr ? TRACK_BIT : 0u);   // big rows: chunked discharge
   }
   if (claimed) fs.add(tr, deg);
 }
@@ -432,8 +494,14 @@ __device__ __forceinline__ void claim_one(const Dev &d, Stage &st, const BfsCtx 
     for (int32_t k = 0; k < nch; k++) c.next.cq[pos + k] = chunk_entry(v, tr ? TRACK_BIT : 0u, k);
   }
   if (c.collect && act) {
+    d.inq[v] = 1;
     const int wb = wl_bin(deg);
-    stage_one(st, 2 + wb, c.wl.bin(wb), c.wl.c + wb, val);
+    if (wb < 2) stage_one(st, 2 + wb, c.wl.bin(wb), c.wl.c + wb, val);
+    else {
+      const int32_t nch = (deg + CH - 1) / CH;
+      const int32_t pos = atomicAdd(c.wl.c + 3, nch);
+      for (int32_t k = 0; k < nch; k++) c.wl.cq[pos + k] = chunk_entry(v, tr ? TRACK_BIT : 0u, k);
+    }
   }
   fs.add(tr, deg);
 }
@@ -644,7 +712,7 @@ __device__ __forceinline__ void bfs_bottom_up_b(const Dev &d, const G &g, Smem &
 // TILE_ITEMS vertices; per tile, warps reserve positions with shared-memory atomics
 // and thread 0 reserves each list's global range with ONE atomic.  Categories:
 // 0,1 = frontier bins 0/1, 2 = frontier chunks (several entries per vertex),
-// 3..6 = worklist bins 0..3.  `classify(v, tr, front, act)` decides for vertex v.
+// 3,4 = worklist bins 0/1, 5 = worklist chunks (vertices of > BIN1_MAX slots).  `classify(v, tr, front, act)` decides for vertex v.
 template <class Classify>
 __device__ __forceinline__ void compact_domain(const Dev &d, TileSm &ts, int32_t N, const int32_t *dom,
                                                const BL &next, const BL &wl, bool collect, Classify classify,
@@ -672,7 +740,8 @@ __device__ __forceinline__ void compact_domain(const Dev &d, TileSm &ts, int32_t
         if (front || act) deg = d.row[v + 1] - d.row[v];
       }
       const int fb = front ? (deg <= BIN0_MAX ? 0 : (deg <= BIN1_MAX ? 1 : 2)) : -1;
-      const int wb = (collect && act) ? (deg <= BIN0_MAX ? 0 : (deg <= BIN1_MAX ? 1 : (deg <= BIN2_MAX ? 2 : 3))) : -1;
+      const int wb = (collect && act) ? (deg <= BIN0_MAX ? 0 : (deg <= BIN1_MAX ? 1 : 2)) : -1;
+      if (wb >= 0) d.inq[v] = 1;
       if (front) { if (tr) fs1 += deg; else fs0 += deg; }
       vv[j] = v; fc[j] = (int8_t)fb; wc[j] = (int8_t)wb; tg[j] = tr ? TRACK_BIT : 0u;
       fo[j] = 0; wo[j] = 0;
@@ -698,10 +767,10 @@ __device__ __forceinline__ void compact_domain(const Dev &d, TileSm &ts, int32_t
         bs = __shfl_sync(0xffffffffu, bs, 0);
         if (fb == 2) fo[j] = bs + ex;
       }
-      // worklist bins
+      // worklist bins 0/1, chunks
       if (collect) {
 #pragma unroll
-        for (int b = 0; b < 4; b++) {
+        for (int b = 0; b < 2; b++) {
           const unsigned m = __ballot_sync(0xffffffffu, wb == b);
           if (m) {
             int bs = 0;
@@ -710,13 +779,22 @@ __device__ __forceinline__ void compact_domain(const Dev &d, TileSm &ts, int32_t
             if (wb == b) wo[j] = bs + __popc(m & ((1u << lane) - 1u));
           }
         }
+        const int32_t wch = wb == 2 ? (deg + CH - 1) / CH : 0;
+        if (__ballot_sync(0xffffffffu, wch > 0)) {
+          long long tot;
+          const int32_t ex = (int32_t)g.exscan(wch, tot);
+          int bs = 0;
+          if (lane == 0) bs = atomicAdd(&ts.cnt[5], (int32_t)tot);
+          bs = __shfl_sync(0xffffffffu, bs, 0);
+          if (wb == 2) wo[j] = bs + ex;
+        }
       }
     }
     __syncthreads();
-    if (threadIdx.x < 7) {
+    if (threadIdx.x < 6) {
       const int32_t cc = ts.cnt[threadIdx.x];
       const int k = threadIdx.x;     // categories -> global counters
-      int32_t *gc = k == 0 ? next.c : k == 1 ? next.c + 1 : k == 2 ? next.c + 3 : wl.c + (k - 3);
+      int32_t *gc = k == 0 ? next.c : k == 1 ? next.c + 1 : k == 2 ? next.c + 3 : k == 5 ? wl.c + 3 : wl.c + (k - 3);
       ts.base[threadIdx.x] = cc ? atomicAdd(gc, cc) : 0;
     }
     __syncthreads();
@@ -726,10 +804,73 @@ __device__ __forceinline__ void compact_domain(const Dev &d, TileSm &ts, int32_t
       if (fc[j] == 0 || fc[j] == 1) next.bin(fc[j])[ts.base[fc[j]] + fo[j]] = e;
       else if (fc[j] == 2)
         for (int32_t k = 0; k < nchv[j]; k++) next.cq[ts.base[2] + fo[j] + k] = chunk_entry(vv[j], tg[j], k);
-      if (wc[j] >= 0) wl.bin(wc[j])[ts.base[3 + wc[j]] + wo[j]] = e;
+      if (wc[j] == 0 || wc[j] == 1) wl.bin(wc[j])[ts.base[3 + wc[j]] + wo[j]] = e;
+      else if (wc[j] == 2) {
+        const int32_t deg = d.row[vv[j] + 1] - d.row[vv[j]];
+        for (int32_t k = 0; k < (deg + CH - 1) / CH; k++) wl.cq[ts.base[5] + wo[j] + k] = chunk_entry(vv[j], tg[j], k);
+      }
     }
     __syncthreads();
   }
+}
+
+__device__ __forceinline__ int32_t *act_buf(Smem &sm) { return &sm.st.f[0][0]; }
+__device__ __forceinline__ int32_t *rel_buf(Smem &sm) { return &sm.st.w[0][0]; }
+
+// block-wide: move `cnt` staged entries (vertex | track tag) into the binned list bl
+// (bins 0/1, chunk entries for bigger rows when bl is chunked, else bins 2/3): one
+// global atomic per category per CTA.  Uses sm.ts; callers pass a block-uniform cnt.
+__device__ __forceinline__ void vflush(const Dev &d, TileSm &ts, const int32_t *buf, int32_t cnt, const BL &bl) {
+  for (int32_t t0 = 0; t0 < cnt; t0 += NT) {
+    if (threadIdx.x < 4) ts.cnt[threadIdx.x] = 0;
+    __syncthreads();
+    const int32_t x = t0 + threadIdx.x;
+    int32_t e = 0, cat = -1, nch = 0, off = 0;
+    if (x < cnt) {
+      e = buf[x];
+      const int32_t v = (int32_t)((uint32_t)e & ~TRACK_BIT);
+      const int32_t deg = d.row[v + 1] - d.row[v];
+      cat = deg <= BIN0_MAX ? 0 : (deg <= BIN1_MAX ? 1 : (deg <= BIN2_MAX ? 2 : 3));
+      if (cat >= 2 && bl.cq) { cat = 3; nch = (deg + CH - 1) / CH; }
+      off = atomicAdd(&ts.cnt[cat], nch ? nch : 1);
+    }
+    __syncthreads();
+    if (threadIdx.x < 4) ts.base[threadIdx.x] = ts.cnt[threadIdx.x] ? atomicAdd(bl.c + threadIdx.x, ts.cnt[threadIdx.x]) : 0;
+    __syncthreads();
+    if (cat >= 0) {
+      if (nch) {
+        const int32_t v = (int32_t)((uint32_t)e & ~TRACK_BIT);
+        for (int32_t k = 0; k < nch; k++) bl.cq[ts.base[3] + off + k] = chunk_entry(v, (uint32_t)e & TRACK_BIT, k);
+      } else {
+        bl.bin(cat)[ts.base[cat] + off] = e;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// block-wide, end of a discharge round: flush the staged activations / relabels
+__device__ __forceinline__ void dis_flush(const Dev &d, Smem &sm, const BL &nxt, const BL &rl) {
+  // activation candidates: every thread's reductions are performed before any check
+  __threadfence();
+  __syncthreads();
+  {
+    const int32_t c = min(sm.ccnt, CCAP);
+    for (int32_t x = threadIdx.x; x < c; x += NT) {
+      const uint32_t e = (uint32_t)sm.cand[x];
+      const int tr = (e & TRACK_BIT) ? 1 : 0;
+      const int32_t v = (int32_t)(e & ~TRACK_BIT);
+      const Track k = make_track(d, tr);
+      if (ldv(d.e + v) * k.sign > 0) activate(d, k, nxt, v, e & TRACK_BIT, sm);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) sm.ccnt = 0;
+  const int32_t a = min(sm.acnt, ACAP), r = min(sm.rcnt, RCAP);
+  __syncthreads();
+  if (threadIdx.x == 0) { sm.acnt = 0; sm.rcnt = 0; }
+  vflush(d, sm.ts, act_buf(sm), a, nxt);
+  vflush(d, sm.ts, rel_buf(sm), r, rl);
 }
 
 // block-wide: flush the stages and publish the per-CTA frontier slot sums
@@ -825,7 +966,7 @@ __device__ __forceinline__ void discharge(const Dev &d, const G &g, Smem &sm, in
     }
     for (int32_t i0 = beg + g.rank(); i0 < end; i0 += 4 * G::size) {
       if (G::size == 1 ? remaining <= 0 : *((volatile long long *)bud) <= 0) break;
-      int32_t r[4], v[4], h[4];
+      int32_t r[4], v[4], h[4], ri[4];
 #pragma unroll
       for (int j = 0; j < 4; j++) {     // independent loads first (ILP), then the gathers
         const int32_t i = i0 + j * G::size;
@@ -833,7 +974,10 @@ __device__ __forceinline__ void discharge(const Dev &d, const G &g, Smem &sm, in
         v[j] = i < end ? d.dst[i] : 0;
       }
 #pragma unroll
-      for (int j = 0; j < 4; j++) h[j] = r[j] > 0 ? ldv(k.hgt + v[j]) : 0;
+      for (int j = 0; j < 4; j++) {     // neighbour height + the reverse slot, in the same wave
+        h[j] = r[j] > 0 ? ldv(k.hgt + v[j]) : 0;
+        ri[j] = r[j] > 0 ? d.rev[i0 + j * G::size] : 0;
+      }
       long long take[4];
 #pragma unroll
       for (int j = 0; j < 4; j++) {       // budget claims
@@ -848,26 +992,10 @@ __device__ __forceinline__ void discharge(const Dev &d, const G &g, Smem &sm, in
         if (r[j] > 0 && take[j] < r[j])
           nmin = (unsigned long long)(uint32_t)h[j] < nmin ? (unsigned long long)(uint32_t)h[j] : nmin;
       }
-      long long oe[4];
 #pragma unroll
-      for (int j = 0; j < 4; j++) {       // all pushes of the step issued before any result is used
-        oe[j] = 0;
+      for (int j = 0; j < 4; j++) {       // pushes: fire-and-forget
         if (take[j] > 0) {
-          const int32_t i = i0 + j * G::size;
-          const int32_t ri = d.rev[i];
-          atomicSub(k.F + i, (int32_t)take[j]);      // c_f(u,v^) -= d
-          atomicSub(k.R + ri, (int32_t)take[j]);     //   mirror
-          atomicAdd(k.F + ri, (int32_t)take[j]);     // c_f(v^,u) += d
-          atomicAdd(k.R + i, (int32_t)take[j]);      //   mirror
-          oe[j] = (long long)atomicAdd(reinterpret_cast<unsigned long long *>(d.e + v[j]),
-                                       (unsigned long long)(take[j] * k.sign));   // e(v^) += d
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < 4; j++) {
-        if (take[j] > 0) {
-          const long long eo = oe[j] * k.sign;
-          if (eo <= 0 && eo + take[j] > 0) activate(d, k, nxt, v[j], tag, sm);
+          push_slot(d, k, nxt, i0 + j * G::size, ri[j], v[j], (int32_t)take[j], tag, sm);
           pushes++;
         }
       }
@@ -910,13 +1038,166 @@ __device__ __forceinline__ void discharge(const Dev &d, const G &g, Smem &sm, in
       atomicMax(&d.ctl->slow, key);
     }
     if (cyc == d.kc && hu < n && eu > 0) activate(d, k, nxt, u, tag, sm);  // KERNELCYCLES spent
-    if (relabelled && d.rlf[u] == 0) { d.rlf[u] = 1; bl_append_one(d, rl, u, tag); }
+    if (relabelled && d.rlf[u] == 0) { d.rlf[u] = 1; stage_relabelled(d, rl, u, tag, sm); }
     atomicAdd(&sm.work, scanned + 16ull * lifts + 16ull);
     sstat_add(sm, ST_DIS_V, 1);
     sstat_add(sm, ST_DIS_SLOTS, scanned);
     sstat_add(sm, ST_RELABELS, lifts);
   }
   sstat_add(sm, ST_PUSHES, pushes);
+}
+
+// ---------------------------------------------------------------------------
+// Chunked discharge of a big vertex u (> BIN1_MAX slots): one cycle of Alg.2 / Alg.6
+// per round, its row split into CH-slot chunks that warps anywhere on the grid take
+// in parallel (a hub no longer serialises a round behind one CTA).
+//  * The chunks claim u's excess directly from e(u): one warp-aggregated atomic per
+//    step takes the admissible residual of the step; whatever e(u) could not cover is
+//    refunded at once, and the chunk is then "dry" (stops scanning: excess gone).
+//  * Each chunk folds the lowest height among its slots left residual into dmin[u]
+//    (0 when dry: an admissible slot may remain) and counts itself in dcnt[u].
+//  * The LAST chunk to finish decides, as Alg.2 l.20-22 does after the pushes: if u
+//    still has excess and every residual slot is at height >= h(u), lift u to
+//    min(dmin + 1, |V|) (R4/R5); if excess remains below |V|, re-queue u.  It resets
+//    dcnt / dmin / inq for the next round and re-reads e(u) after clearing inq, so an
+//    activation that lost to the stale flag is not lost.
+// Heights of u are read once per round; stale neighbour heights cost work only (RIE
+// and the fresh BFS of R9 repair them), exactly as in the one-group discharge.
+__device__ __forceinline__ void discharge_chunk(const Dev &d, Smem &sm, long long ce, const BL &rl, const BL &nxt) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t lo = (uint32_t)ce;
+  const int tr = (lo & TRACK_BIT) ? 1 : 0;
+  const uint32_t tag = tr ? TRACK_BIT : 0u;
+  const int32_t u = (int32_t)(lo & ~TRACK_BIT);
+  const Track k = make_track(d, tr);
+  const int32_t n = d.n;
+  const int32_t rbeg = d.row[u], rend = d.row[u + 1];
+  const int32_t beg = rbeg + (int32_t)(ce >> 32) * CH;
+  const int32_t end = min(rend, beg + CH);
+  const int32_t nch = (rend - rbeg + CH - 1) / CH;
+  const unsigned long long t_start = d.trace ? gtimer() : 0;
+  const int32_t hu = ldv(k.hgt + u);
+  uint32_t nmin = 0xffffffffu;           // lowest height among slots left residual
+  unsigned long long pushes = 0, scanned = 0;
+  bool dry = false;
+  WarpG g{lane};
+  if (hu < n) {
+    for (int32_t b0 = beg; b0 < end; b0 += 128) {   // warp-uniform trip count (collectives inside)
+      const int32_t i0 = b0 + lane;
+      int32_t r[4], v[4], h[4], ri[4];
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        const int32_t i = i0 + j * 32;
+        r[j] = i < end ? ldv(k.F + i) : 0;
+        v[j] = i < end ? d.dst[i] : 0;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        h[j] = r[j] > 0 ? ldv(k.hgt + v[j]) : 0;
+        ri[j] = r[j] > 0 ? d.rev[i0 + j * 32] : 0;
+      }
+      long long asum = 0;
+#pragma unroll
+      for (int j = 0; j < 4; j++) asum += (r[j] > 0 && h[j] < hu) ? r[j] : 0;
+      long long tot;
+      const long long pre = g.exscan(asum, tot);
+      long long got = 0;
+      if (tot > 0) {                       // claim the step's admissible residual from e(u)
+        if (lane == 0) {
+          const long long old = (long long)atomicAdd(reinterpret_cast<unsigned long long *>(d.e + u),
+                                                     (unsigned long long)(-tot * k.sign)) * k.sign;
+          got = old <= 0 ? 0 : (old < tot ? old : tot);
+          if (got < tot) atom_add(d.e + u, (tot - got) * k.sign);   // refund what e(u) did not cover
+        }
+        got = g.bcast(got);
+      }
+      long long mine = got - pre;          // this lane's share, lane order
+      mine = mine < 0 ? 0 : (mine > asum ? asum : mine);
+      long long take[4];
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        take[j] = 0;
+        if (r[j] > 0 && h[j] < hu) { take[j] = mine < r[j] ? mine : r[j]; mine -= take[j]; }
+        if (r[j] > 0 && take[j] < r[j]) nmin = (uint32_t)h[j] < nmin ? (uint32_t)h[j] : nmin;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        if (take[j] > 0) {
+          push_slot(d, k, nxt, i0 + j * 32, ri[j], v[j], (int32_t)take[j], tag, sm);
+          pushes++;
+        }
+      }
+      scanned += 128;
+      if (got < tot) { dry = true; break; }   // u's excess is gone (warp-uniform)
+    }
+  }
+  nmin = (uint32_t)g.min(dry ? 0ull : (unsigned long long)nmin);
+  if (lane == 0) {
+    if (nmin < (uint32_t)DMIN_NONE) atomicMin(d.dmin + u, (int32_t)nmin);
+    __threadfence();
+    const int32_t done = atomicAdd(d.dcnt + u, 1);
+    unsigned long long lifts = 0;
+    if (done == nch - 1) {                 // last chunk of u this round
+      __threadfence();
+      const int32_t mn = atomicExch(d.dmin + u, DMIN_NONE);
+      d.dcnt[u] = 0;
+      atomicExch(d.inq + u, 0);
+      __threadfence();
+      const long long eu = ldv(d.e + u) * k.sign;
+      if (eu > 0 && hu < n) {
+        int32_t nh = hu;
+        if (mn >= hu) nh = mn >= n ? n : mn + 1;   // every residual slot at >= h(u): lift
+        if (nh > hu) {
+          k.hgt[u] = nh;
+          lifts = 1;
+          if (d.rlf[u] == 0) { d.rlf[u] = 1; stage_relabelled(d, rl, u, tag, sm); }
+        }
+        if (nh < n) activate(d, k, nxt, u, tag, sm);
+      }
+      sstat_add(sm, ST_DIS_V, 1);
+      sstat_add(sm, ST_RELABELS, lifts);
+    }
+    if (d.trace) {
+      const unsigned long long dt = gtimer() - t_start;
+      const unsigned long long key = (min(dt, 0xffffffffull) << 32) |
+                                     ((unsigned long long)min(rend - rbeg, 0xffffff) << 8) | 1ull;
+      atomicMax(&d.ctl->slow, key);
+    }
+    atomicAdd(&sm.work, scanned + 16ull * lifts + 16ull);
+    sstat_add(sm, ST_DIS_SLOTS, scanned);
+  }
+  sstat_add(sm, ST_PUSHES, pushes);
+}
+
+// Discharge round: warps take worklist chunks (big vertices) and bin-1 vertices from
+// one index space, 8-lane tiles take bin-0 vertices; the first item of every group is
+// static (group id), later ones are claimed from cl[1] / cl[2] (see process_bl_dyn).
+template <class FnC, class FnW, class FnT>
+__device__ __forceinline__ void process_dis(const BL &bl, const int32_t c[NB], int32_t *cl, FnC chunk, FnW warp1,
+                                            FnT tile0) {
+  {
+    WarpG g{(int)(threadIdx.x & 31)};
+    const int32_t nwi = c[3] + c[1];
+    const int32_t nw = gridDim.x * WPB;
+    int32_t x = blockIdx.x * WPB + (threadIdx.x >> 5);
+    while (x < nwi) {
+      if (x < c[3]) chunk(bl.cq[x]);
+      else warp1(g, bl.bin(1)[x - c[3]]);
+      if (g.lane == 0) x = nw + atomicAdd(cl + 1, 1);
+      x = __shfl_sync(0xffffffffu, x, 0);
+    }
+  }
+  {
+    TileG<8> g((int)(threadIdx.x & 31));
+    const int32_t *b = bl.bin(0);
+    const int32_t ntl = (gridDim.x * NT) >> 3;
+    int32_t x = (blockIdx.x * NT + threadIdx.x) >> 3;
+    while (x < c[0]) {
+      tile0(g, b[x]);
+      if (g.rank() == 0) x = ntl + atomicAdd(cl + 2, 1);
+      x = __shfl_sync(g.mask, x, 0, 8);
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1010,9 +1291,11 @@ struct Lists {      // (members, not arrays: a dynamically indexed array would l
   int32_t *wl0, *wl1;     // worklist ping-pong, [NB bins][n] each
   int32_t *rl;            // relabelled, [NB bins][n]
   long long *rlc;         // its chunk queue
+  long long *cw0, *cw1;   // worklist chunk queues (ping-pong with wl0 / wl1)
   __device__ int32_t *q(int i) const { return i ? q1 : q0; }
   __device__ long long *qc(int i) const { return i ? qc1 : qc0; }
   __device__ int32_t *wl(int i) const { return i ? wl1 : wl0; }
+  __device__ long long *cw(int i) const { return i ? cw1 : cw0; }
 };
 
 
@@ -1033,7 +1316,7 @@ struct Lists {      // (members, not arrays: a dynamically indexed array would l
 __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseClock &clk, int kind,
                             bool collect, bool stage2, bool warm = false) {
   const size_t nb = (size_t)NB * d.n;
-  const Lists L{d.q0, d.q1, d.cq0, d.cq1, d.wl, d.wl + nb, d.rl, d.cqr};
+  const Lists L{d.q0, d.q1, d.cq0, d.cq1, d.wl, d.wl + nb, d.rl, d.cqr, d.cw0, d.cw1};
   const int32_t n = d.n;
   Ctl *ctl = d.ctl;
   int32_t *qc = ctl->qc, *wlc = ctl->wlc, *rlc = ctl->rlc;
@@ -1060,7 +1343,7 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
       FS fs;
       long long mu0 = 0, mu1 = 0;
       const BfsCtx c0{0, false, 0u, 0u, BL{L.q0, qc, n, L.qc0},
-                      BL{L.wl0, wlc, n, nullptr}, ctl->fs};
+                      BL{L.wl0, wlc, n, L.cw0}, ctl->fs};
       for (int32_t b = blockIdx.x * NT + (threadIdx.x & ~31); b < N; b += nt) {
         const int32_t x = b + (threadIdx.x & 31);
         bool r0 = false, r1 = false, in0 = false, in1 = false;
@@ -1142,7 +1425,7 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
       const bool dn1 = !bu1 && f1 > 0 && (unsigned long long)f1 * DENSE_DIV >= (unsigned long long)d.S;
       const BfsCtx ctx{lvl, collect, (bu0 ? 1u : 0u) | (bu1 ? 2u : 0u), (dn0 ? 1u : 0u) | (dn1 ? 2u : 0u),
                        BL{L.q((lvl + 1) & 1), qc + NB * ((lvl + 1) % 3), n, L.qc((lvl + 1) & 1)},
-                       BL{L.wl0, wlc, n, nullptr}, ctl->fs + 2 * ((lvl + 1) % 3)};
+                       BL{L.wl0, wlc, n, L.cw0}, ctl->fs + 2 * ((lvl + 1) % 3)};
       if (lead && (bu0 || bu1)) sstat_add(sm, ST_BU_LEVELS, 1);
       bfs_expand_level(d, grid, sm, sm.st, clk, iter, BL{L.q(lvl & 1), cur_c, n, L.qc(lvl & 1)}, c, ctx, d.bul,
                        ctl->bulc + 2 * (lvl & 1));
@@ -1195,10 +1478,12 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
         if (threadIdx.x < 3) ctl->claim[3 * nn + threadIdx.x] = 0;   // claimed in round r-1
         if (threadIdx.x == 0) ctl->work[nx] = 0;  // last read at the end of round r-2; filled in round r+1
       }
-      const BL nxt{L.wl((r + 1) & 1), wlc + NB * nx, n, nullptr};
-      process_bl_dyn(BL{L.wl(r & 1), wlc + NB * cur, n, nullptr}, w, sm, ctl->claim + 3 * cur,
-                     [&](auto &g, int32_t entry) { discharge(d, g, sm, entry, rl, nxt, ctl->work + cur); });
-      __syncthreads();
+      const BL nxt{L.wl((r + 1) & 1), wlc + NB * nx, n, L.cw((r + 1) & 1)};
+      process_dis(BL{L.wl(r & 1), wlc + NB * cur, n, L.cw(r & 1)}, w, ctl->claim + 3 * cur,
+                  [&](long long ce) { discharge_chunk(d, sm, ce, rl, nxt); },
+                  [&](const WarpG &g, int32_t entry) { discharge(d, g, sm, entry, rl, nxt, ctl->work + cur); },
+                  [&](const TileG<8> &g, int32_t entry) { discharge(d, g, sm, entry, rl, nxt, ctl->work + cur); });
+      dis_flush(d, sm, nxt, rl);
       if (threadIdx.x == 0 && sm.work) { atomicAdd(ctl->work + cur, sm.work); sm.work = 0; }
       if (lead) sstat_add(sm, ST_ROUNDS, 1);
       gsync(d, grid, sm);
@@ -1216,11 +1501,13 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
       if (total(wn) == 0) break;
       if (r + 1 >= MAX_ROUNDS || (long long)spent > d.work_budget) {   // hand the rest to a global relabel
         if (lead) sstat_add(sm, ST_BUDGET_STOPS, 1);
-        for (int b = 0; b < NB; b++) {
+        for (int b = 0; b < 2; b++) {
           const int32_t *lst = nxt.bin(b);
           for (int32_t x = blockIdx.x * NT + threadIdx.x; x < wn[b]; x += nt)
             d.inq[(uint32_t)lst[x] & ~TRACK_BIT] = 0;
         }
+        for (int32_t x = blockIdx.x * NT + threadIdx.x; x < wn[3]; x += nt)
+          d.inq[(uint32_t)nxt.cq[x] & ~TRACK_BIT] = 0;
         break;                                    // (the RIE barrier below publishes the flags)
       }
     }
@@ -1278,7 +1565,7 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(const __grid_con
   __shared__ Smem sm;
   for (int i = threadIdx.x; i < ST_N; i += NTHREADS) sm.stat[i] = 0;
   if (threadIdx.x < 6) sm.st.cnt[threadIdx.x] = 0;
-  if (threadIdx.x == 0) { sm.work = 0; sm.tprev = gtimer(); }
+  if (threadIdx.x == 0) { sm.work = 0; sm.tprev = gtimer(); sm.acnt = 0; sm.rcnt = 0; sm.ccnt = 0; }
   __syncthreads();
   const int32_t n = d.n;
   const int32_t gt = blockIdx.x * NTHREADS + threadIdx.x, nt = gridDim.x * NTHREADS;
@@ -1348,7 +1635,7 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(const __grid_con
       // Warm start of Alg.8 stage 1: only batch endpoints changed excess, so the
       // new roots (T-deficits for h+, S-excess for h-, Alg.8 l.16-24) drop to 0 and
       // the active ones seed round 0's worklist (ring slot 0, deduplicated by inq)
-      const BL wl0{d.wl, ctl->wlc, n, nullptr};
+      const BL wl0{d.wl, ctl->wlc, n, d.cw0};
       for (int64_t j = gt; j < 2 * d.k; j += nt) {
         const int32_t x = (j & 1) ? d.bv[j >> 1] : d.bu[j >> 1];
         if (x == d.s || x == d.t) continue;
@@ -1356,17 +1643,15 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(const __grid_con
         const long long ev = ldv(d.e + x);
         if (p == PART_T) {
           if (ev < 0) d.hp[x] = 0;
-          else if (ev > 0 && ldv(d.hp + x) < n && atomicCAS(d.inq + x, 0, 1) == 0) {
-            bl_append_one(d, wl0, x, 0u);
-            sstat_add(sm, ST_ACTIVATIONS, 1);
-          }
+          else if (ev > 0 && ldv(d.hp + x) < n) activate(d, make_track(d, 0), wl0, x, 0u, sm);
         } else if (p == PART_S) {
           if (ev > 0) d.hm[x] = 0;
-          else if (ev < 0 && ldv(d.hm + x) < n && atomicCAS(d.inq + x, 0, 1) == 0) {
-            bl_append_one(d, wl0, x, TRACK_BIT);
-            sstat_add(sm, ST_ACTIVATIONS, 1);
-          }
+          else if (ev < 0 && ldv(d.hm + x) < n) activate(d, make_track(d, 1), wl0, x, TRACK_BIT, sm);
         }
+      }
+      {
+        const BL none{d.rl, ctl->rlc, n, d.cqr};    // (no relabels staged here)
+        dis_flush(d, sm, wl0, none);
       }
       gsync(d, grid, sm);
       clk.lap(d, sm, ST_T_PRO, 0, 3, (int32_t)d.k);
@@ -1400,14 +1685,20 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(const __grid_con
       ctl->qc[threadIdx.x] = 0;
       if (threadIdx.x < 2) { ctl->fs[threadIdx.x] = 0; ctl->mu[threadIdx.x] = 0; }
     }
-    for (int32_t b = blockIdx.x * NTHREADS + (threadIdx.x & ~31); b < n; b += nt) {
-      const int32_t v = b + (threadIdx.x & 31);
-      bool inP = false;
-      if (v < n) {
-        inP = d.row[v + 1] > d.row[v] && ldv(d.hp + v) >= n && ldv(d.hm + v) >= n;
-        if (inP) d.part[v] = PART_P;
+    for (int32_t v = gt; v < n; v += nt) {         // block-staged appends (one global atomic per CTA)
+      if (d.row[v + 1] > d.row[v] && ldv(d.hp + v) >= n && ldv(d.hm + v) >= n) {
+        d.part[v] = PART_P;
+        const int32_t pos = atomicAdd(&sm.acnt, 1);
+        if (pos < ACAP) act_buf(sm)[pos] = v;
+        else d.plist[atomicAdd(&ctl->pcnt, 1)] = v;
       }
-      warp_append(inP, v, d.plist, &ctl->pcnt);
+    }
+    __syncthreads();
+    {
+      const int32_t c = min(sm.acnt, ACAP);
+      if (threadIdx.x == 0) { sm.ts.base[0] = c ? atomicAdd(&ctl->pcnt, c) : 0; sm.acnt = 0; }
+      __syncthreads();
+      for (int32_t x = threadIdx.x; x < c; x += NTHREADS) d.plist[sm.ts.base[0] + x] = act_buf(sm)[x];
     }
     gsync(d, grid, sm);
     const int32_t pc = cta_ld(sm, &ctl->pcnt);
