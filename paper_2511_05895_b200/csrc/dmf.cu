@@ -66,6 +66,11 @@ struct dmf_graph {
   int32_t *plist = nullptr, *stamp = nullptr, *inq = nullptr, *bul = nullptr;
   long long *cq0 = nullptr, *cq1 = nullptr, *cqr = nullptr, *cw0 = nullptr, *cw1 = nullptr;
   int32_t *dcnt = nullptr, *dmin = nullptr;
+  long long *aq = nullptr;
+  int32_t aq_mask = 0;
+  bool async = true;         // DMF_ASYNC=0: barrier-separated discharge rounds
+  int32_t async_warps = 8;   // DMF_ASYNC_WARPS
+  long long budget_mul = 1;  // DMF_BUDGET_MUL: discharge work between global relabels, in whole-graph BFS units
   long long *e = nullptr;
   uint8_t *part = nullptr, *mask = nullptr, *rlf = nullptr;
   int32_t *bbuf = nullptr;   // batch staging: u, v, c, slot  (4 * bcap)
@@ -216,7 +221,7 @@ static Dev make_dev(dmf_graph *g) {
   d.max_iters = g->opt.max_iters > 0 ? g->opt.max_iters : (int32_t)(4LL * g->n + 64 > 0x3fffffff ? 0x3fffffff : 4LL * g->n + 64);
   d.batch_id = g->batch_id;
   d.warm = g->warm ? 1 : 0;
-  d.work_budget = g->S + 6LL * g->n;     // ~ the cost of one whole-graph global relabel
+  d.work_budget = (g->S + 6LL * g->n) * g->budget_mul;   // ~ the cost of one whole-graph global relabel
   d.S = g->S; d.k = 0;
   d.row = g->row; d.dst = g->dst; d.rev = g->rev; d.cap = g->cap; d.res = g->res; d.rres = g->rres;
   d.e = g->e; d.hp = g->hp; d.hm = g->hm; d.part = g->part;
@@ -224,6 +229,8 @@ static Dev make_dev(dmf_graph *g) {
   d.wl = g->wl; d.rl = g->rl; d.inq = g->inq; d.bul = g->bul; d.rlf = g->rlf;
   d.cq0 = g->cq0; d.cq1 = g->cq1; d.cqr = g->cqr; d.cw0 = g->cw0; d.cw1 = g->cw1;
   d.dcnt = g->dcnt; d.dmin = g->dmin;
+  d.aq = g->aq; d.aq_mask = g->aq_mask; d.async = g->async ? 1 : 0;
+  d.async_warps = g->async_warps;
   d.plist = g->plist; d.stamp = g->stamp;
   d.mask = g->mask; d.ctl = g->ctl;
   d.dbg = g->ddbg;
@@ -292,6 +299,7 @@ static int run_solve(dmf_graph *g, int32_t mode, const Dev &dv) {
   st.t_epilogue_us = c.stat[ST_T_EPI] * 1e-3f;
   st.batch_entries = dv.k;
   st.device_ms = ms;
+  if (c.pad != 0) fprintf(stderr, "[dmf debug] vertex %d discharged concurrently\n", c.pad - 1);
   if (c.status != 0) {
     const char *what = c.status == DMF_ENOSLOT ? "no slot for (u,v)"
                      : c.status == DMF_EDUP ? "duplicate (u,v) in batch"
@@ -435,17 +443,28 @@ int dmf_create(int32_t n, const int64_t *row_ptr, const int32_t *col, const int3
   g->cw1 = (long long *)g->alloc(cqn * 8);
   g->dcnt = (int32_t *)g->alloc(nn * 4);
   g->dmin = (int32_t *)g->alloc(nn * 4);
+  {
+    // live ring window <= queued items (<= n + S/CH, inq-deduplicated) + one outstanding
+    // claim per warp of the grid (idle warps claim ahead of the tail): no index aliases
+    size_t cap = 1024;
+    while (cap < 2 * cqn + 65536) cap <<= 1;
+    g->aq = (long long *)g->alloc(cap * 8);
+    g->aq_mask = (int32_t)(cap - 1);
+  }
   g->rl = (int32_t *)g->alloc(NB * nn * 4);
   g->plist = (int32_t *)g->alloc(nn * 4);
   g->ctl = (Ctl *)g->alloc(sizeof(Ctl));
   if (!g->row || !g->dst || !g->rev || !g->cap || !g->res || !g->rres || !g->stamp || !g->e || !g->hp || !g->hm ||
       !g->part || !g->mask || !g->q0 || !g->q1 || !g->wl || !g->rl || !g->plist || !g->ctl || !g->inq || !g->rlf || !g->bul || !g->cq0 || !g->cq1 || !g->cqr ||
-      !g->cw0 || !g->cw1 || !g->dcnt || !g->dmin) {
+      !g->cw0 || !g->cw1 || !g->dcnt || !g->dmin || !g->aq) {
     fail(DMF_ENOMEM, "device allocation failed (state, S=%lld)", (long long)S);
     return bail(DMF_ENOMEM);
   }
   CKB(cudaMallocHost((void **)&g->hctl, sizeof(Ctl)));
   if (const char *nw = getenv("DMF_NO_WARM")) g->no_warm = atoi(nw) != 0;
+  if (const char *as = getenv("DMF_ASYNC")) g->async = atoi(as) != 0;
+  if (const char *aw = getenv("DMF_ASYNC_WARPS")) g->async_warps = atoi(aw) > 0 ? (atoi(aw) < WPB ? atoi(aw) : WPB) : 8;
+  if (const char *bm = getenv("DMF_BUDGET_MUL")) g->budget_mul = atoll(bm) > 0 ? atoll(bm) : 1;
   if (const char *wd = getenv("DMF_WATCHDOG_S")) {
     g->watchdog_s = atof(wd);
     CKB(cudaHostAlloc((void **)&g->hdbg, 64, cudaHostAllocMapped));
@@ -456,6 +475,7 @@ int dmf_create(int32_t n, const int64_t *row_ptr, const int32_t *col, const int3
   CKB(cudaMemsetAsync(g->rlf, 0, nn, st));
   CKB(cudaMemsetAsync(g->dcnt, 0, nn * 4, st));
   CKB(cudaMemsetAsync(g->dmin, 0x7f, nn * 4, st));   // DMIN_NONE
+  CKB(cudaMemsetAsync(g->aq, 0xff, ((size_t)g->aq_mask + 1) * 8, st));   // AQ_EMPTY
   if (S) {
     CKB(cudaMemsetAsync(err, 0, 64, st));
     k_rows<<<blocks(nn + 1), TB, 0, st>>>(n, S, ukey, g->row);

@@ -29,6 +29,7 @@ constexpr uint32_t TRACK_BIT = 0x80000000u;
 
 // dmin sentinel (memset byte 0x7f): above every height (heights are <= |V|+1 < 2^31-1)
 constexpr int32_t DMIN_NONE = 0x7f7f7f7f;
+constexpr long long AQ_EMPTY = -1;
 
 // Partition labels of Alg.8.  S'/T' are stored as S/T.
 enum : uint8_t { PART_NONE = 0, PART_S = 1, PART_T = 2, PART_P = 3 };
@@ -66,6 +67,11 @@ struct Ctl {
   int32_t bulc[4];              // bottom-up candidate queue counts [level & 1][warp/CTA bin]
   unsigned long long mu[2];     // slots of the still-unlabelled vertices per track (BFS direction choice)
   unsigned long long stat[ST_N];
+  // asynchronous discharge phase: ring queue of activations
+  unsigned long long aw;        // (ring tail << 32) | items pending (queued or in progress)
+  int32_t ahead;                // next item index to claim (initial worklist first, then the ring)
+  int32_t astop;                // work budget spent: stop claiming
+  unsigned long long awork;     // discharge work of the phase
 };
 
 // Everything a kernel needs, passed by value.  Slot arrays are SoA int32[S]:
@@ -99,6 +105,10 @@ struct Dev {
   long long *cw0, *cw1;      // chunk queues of the discharge worklist ping-pong (vertices of > BIN1_MAX slots)
   int32_t *dcnt;             // chunked discharge: chunks of u finished in the current round
   int32_t *dmin;             // chunked discharge: lowest height among u's slots left residual (DMIN_NONE if none)
+  long long *aq;             // asynchronous discharge ring (AQ_EMPTY when free), aq_mask + 1 entries
+  int32_t aq_mask;
+  int32_t async;             // 1: asynchronous discharge phase, 0: barrier-separated rounds
+  int32_t async_warps;       // consumer warps per CTA in the asynchronous phase
   int32_t *plist;            // region P of push-pull stage 2
   int32_t *stamp;            // per-slot batch stamp (duplicate detection)
   const int32_t *bu, *bv, *bc;  // batch entries

@@ -63,6 +63,9 @@ struct Smem {
   long long cv[8];                 // control words snapped once per CTA (cta_snap)
   int32_t acnt, rcnt;              // discharge: staged activations / relabelled vertices (in st.f / st.w)
   int32_t ccnt;                    // discharge: staged push heads (activation candidates)
+  int32_t wcc[WPB];                // async discharge: per-warp candidate counts (warp w: cand[w*WCAP..])
+  int32_t astop;                   // async discharge: this CTA has seen ctl->astop
+  unsigned long long apoll;        // async discharge: last global poll of ctl->astop
   int32_t cand[2048];
   Stage st;                    // block-staged appends (BFS)
   TileSm ts;                   // tiled compaction (dense top-down BFS levels)
@@ -302,14 +305,41 @@ constexpr int32_t RCAP = 4 * SW;     // staged relabelled vertices per CTA
 __device__ __forceinline__ int32_t *act_buf(Smem &sm);
 __device__ __forceinline__ int32_t *rel_buf(Smem &sm);
 
+#ifdef DMF_DEBUG_BUSY
+__device__ __forceinline__ void dbg_rec(const Dev &d, int32_t kind, int32_t a, int32_t b, int32_t c, int32_t e5) {
+  if (!d.trace) return;
+  const int32_t r = atomicAdd(&d.ctl->ntrace, 1);
+  if (r >= d.trace_cap) return;
+  int32_t *p = d.trace + 8 * r;
+  p[0] = kind; p[1] = a; p[2] = (int32_t)(blockIdx.x * WPB + (threadIdx.x >> 5)); p[3] = b; p[4] = c; p[5] = e5;
+  p[6] = (int32_t)(gtimer() & 0x7fffffff); p[7] = 0;
+}
+#define DBG(...) dbg_rec(__VA_ARGS__)
+#else
+#define DBG(...)
+#endif
+// Asynchronous discharge: append v (every CH-slot chunk of a big row) to the ring.  One
+// atomic reserves the ring positions AND counts the items as pending, so a consumer
+// can never finish an item before it is counted.
+__device__ __forceinline__ void async_enqueue(const Dev &d, int32_t v, uint32_t tag) {
+  const int32_t deg = d.row[v + 1] - d.row[v];
+  const int32_t nch = deg > BIN1_MAX ? (deg + CH - 1) / CH : 1;
+  const unsigned long long old = atomicAdd(&d.ctl->aw, ((unsigned long long)nch << 32) | (unsigned long long)nch);
+  const uint32_t pos = (uint32_t)(old >> 32);
+  DBG(d, 202, v, (int32_t)pos, (int32_t)(uint32_t)old, nch);
+  for (int32_t k = 0; k < nch; k++)
+    *(volatile long long *)(d.aq + ((pos + (uint32_t)k) & (uint32_t)d.aq_mask)) = chunk_entry(v, tag, k);
+}
+
 __device__ __forceinline__ void activate(const Dev &d, const Track &k, const BL &nxt, int32_t v, uint32_t tag,
-                                         Smem &sm) {
+                                         Smem &sm, bool ring = true) {
   if (v == d.s || v == d.t) return;
   if (atomicCAS(d.inq + v, 0, 1) != 0) return;     // (a vertex at height >= |V| exits at once)
+  sstat_add(sm, ST_ACTIVATIONS, 1);
+  if (d.async && ring) { async_enqueue(d, v, tag); return; }
   const int32_t pos = atomicAdd(&sm.acnt, 1);
   if (pos < ACAP) act_buf(sm)[pos] = (int32_t)((uint32_t)v | tag);
   else bl_append_one(d, nxt, v, tag);
-  sstat_add(sm, ST_ACTIVATIONS, 1);
 }
 // One push of d on slot i = (u,v) of track k (ri = rev[i]): the four residual updates and
 // e(v) += d are fire-and-forget reductions; v is staged as an activation CANDIDATE that
@@ -317,6 +347,7 @@ __device__ __forceinline__ void activate(const Dev &d, const Track &k, const BL 
 // every push), so no push waits for an atomic's return.  Candidate overflow falls back
 // to the returning atomic and the 0-crossing test.
 constexpr int32_t CCAP = 2048;
+constexpr int32_t WCAP = CCAP / WPB;   // async: per-warp candidate slots
 __device__ __forceinline__ void push_slot(const Dev &d, const Track &k, const BL &nxt, int32_t i, int32_t ri, int32_t v,
                                           int32_t take, uint32_t tag, Smem &sm);
 
@@ -332,10 +363,13 @@ __device__ __forceinline__ void push_slot(const Dev &d, const Track &k, const BL
   atomicSub(k.R + ri, take);         //   mirror
   atomicAdd(k.F + ri, take);         // c_f(v,u) += d
   atomicAdd(k.R + i, take);          //   mirror
-  const int32_t pos = atomicAdd(&sm.ccnt, 1);
-  if (pos < CCAP) {
+  // rounds: one list per CTA, checked at the round end; async: one list per warp,
+  // checked after the warp's item (async_candidates)
+  const int w = (int)(threadIdx.x >> 5);
+  const int32_t pos = d.async ? atomicAdd(&sm.wcc[w], 1) : atomicAdd(&sm.ccnt, 1);
+  if (pos < (d.async ? WCAP : CCAP)) {
     atom_add(d.e + v, (long long)take * k.sign);                           // e(v) += d
-    sm.cand[pos] = (int32_t)((uint32_t)v | tag);
+    sm.cand[d.async ? w * WCAP + pos : pos] = (int32_t)((uint32_t)v | tag);
   } else {
     const long long eo = (long long)atomicAdd(reinterpret_cast<unsigned long long *>(d.e + v),
                                               (unsigned long long)((long long)take * k.sign)) * k.sign;
@@ -945,9 +979,17 @@ __device__ __forceinline__ void discharge(const Dev &d, const G &g, Smem &sm, in
   const Track k = make_track(d, tr);
   const int32_t n = d.n;
   const int32_t beg = d.row[u], end = d.row[u + 1];
-  if (g.rank() == 0) { d.inq[u] = 0; __threadfence(); }
+  // rounds: clear the queued flag first, so a push into u during this discharge queues
+  // u for the next round.  async: u keeps the flag while it is being discharged (no
+  // second warp may take u concurrently: both would push the same residual) and the
+  // epilogue below clears it and re-checks e(u).
+  if (!d.async && g.rank() == 0) { d.inq[u] = 0; __threadfence(); }
   const unsigned long long t_start = d.trace ? gtimer() : 0;
+#ifdef DMF_DEBUG_BUSY
+  if (g.rank() == 0 && atomicExch(d.dcnt + u, 1) != 0) atomicCAS(&d.ctl->pad, 0, u + 1);
+#endif
   int32_t hu = ldv(k.hgt + u);
+  if (g.rank() == 0) DBG(d, 200, u, (int32_t)ldv(d.e + u), hu, ldv(d.inq + u));
   bool relabelled = false;
   unsigned long long scanned = 0, pushes = 0, lifts = 0;
   long long eu = 0;
@@ -1030,6 +1072,10 @@ __device__ __forceinline__ void discharge(const Dev &d, const G &g, Smem &sm, in
       lifts++;
     }
   }
+  if (d.async) {                        // every member's pushes land before u is released
+    __threadfence();
+    g.sync();
+  }
   if (g.rank() == 0) {
     if (d.trace) {                      // slowest discharge of the round: (ns, degree, cycles)
       const unsigned long long dt = gtimer() - t_start;
@@ -1037,7 +1083,18 @@ __device__ __forceinline__ void discharge(const Dev &d, const G &g, Smem &sm, in
                                      ((unsigned long long)min(end - beg, 0xffffff) << 8) | (unsigned long long)min(cyc, 255);
       atomicMax(&d.ctl->slow, key);
     }
-    if (cyc == d.kc && hu < n && eu > 0) activate(d, k, nxt, u, tag, sm);  // KERNELCYCLES spent
+#ifdef DMF_DEBUG_BUSY
+    DBG(d, 201, u, (int32_t)ldv(d.e + u), hu, pushes);
+    if (atomicExch(d.dcnt + u, 0) != 1) atomicCAS(&d.ctl->pad, 0, -(u + 1));
+    __threadfence();
+#endif
+    if (d.async) {
+      atomicExch(d.inq + u, 0);
+      __threadfence();
+      if (hu < n && ldv(d.e + u) * k.sign > 0) activate(d, k, nxt, u, tag, sm);
+    } else if (cyc == d.kc && hu < n && eu > 0) {
+      activate(d, k, nxt, u, tag, sm);  // KERNELCYCLES spent
+    }
     if (relabelled && d.rlf[u] == 0) { d.rlf[u] = 1; stage_relabelled(d, rl, u, tag, sm); }
     atomicAdd(&sm.work, scanned + 16ull * lifts + 16ull);
     sstat_add(sm, ST_DIS_V, 1);
@@ -1132,6 +1189,8 @@ __device__ __forceinline__ void discharge_chunk(const Dev &d, Smem &sm, long lon
     }
   }
   nmin = (uint32_t)g.min(dry ? 0ull : (unsigned long long)nmin);
+  __threadfence();                       // every lane's pushes land before u can be taken again
+  __syncwarp();
   if (lane == 0) {
     if (nmin < (uint32_t)DMIN_NONE) atomicMin(d.dmin + u, (int32_t)nmin);
     __threadfence();
@@ -1282,6 +1341,123 @@ __device__ __forceinline__ void rie_chunks(const Dev &d, Smem &sm, const long lo
 }
 
 // ---------------------------------------------------------------------------
+// ASYNCHRONOUS discharge phase (replaces the barrier-separated rounds; DMF_ASYNC=0
+// restores them).  Every warp repeatedly claims the next item index: first the
+// worklist the BFS (or the warm start) collected, then the ring into which activate()
+// appends newly active vertices at once, so excess moves on without waiting for a grid
+// barrier per hop.  An item is a vertex of <= BIN1_MAX slots (discharge by the warp,
+// up to KERNELCYCLES cycles) or one chunk of a bigger row (discharge_chunk).
+// Termination: aw's low word counts items queued or in progress (set to the initial
+// worklist size before the phase; every enqueue adds before publishing, every item
+// subtracts after its own enqueues), so it reaches 0 only when no item exists or can
+// appear; the warp that takes it to 0, or one that spends the work budget, raises
+// astop.  Waiting warps poll their ring slot and, at most once per ~1 us per CTA, the
+// flag (through shared memory).  Items left behind by a budget stop are swept (their
+// inq flags cleared) by async_sweep; the next fresh BFS re-collects them (R9).
+__device__ __forceinline__ long long ldvol(const long long *p) { return *(const volatile long long *)p; }
+__device__ __forceinline__ int32_t ldvol(const int32_t *p) { return *(const volatile int32_t *)p; }
+
+__device__ __forceinline__ bool async_stopped(const Dev &d, Smem &sm) {
+  if (sm.astop) return true;
+  const unsigned long long now = gtimer();
+  if (now - sm.apoll > 1000) {             // one global poll per CTA per microsecond
+    sm.apoll = now;
+    if (ldvol(&d.ctl->astop)) { sm.astop = 1; return true; }
+  }
+  return false;
+}
+
+// warp-wide, after an item whose members fenced their pushes: activate the staged heads
+// that hold excess (same rule as dis_flush)
+__device__ __forceinline__ void async_candidates(const Dev &d, Smem &sm, const BL &nxt) {
+  const int w = (int)(threadIdx.x >> 5), lane = threadIdx.x & 31;
+  __syncwarp();
+  const int32_t c = min(sm.wcc[w], WCAP);
+  for (int32_t x = lane; x < c; x += 32) {
+    const uint32_t e = (uint32_t)sm.cand[w * WCAP + x];
+    const int tr = (e & TRACK_BIT) ? 1 : 0;
+    const int32_t v = (int32_t)(e & ~TRACK_BIT);
+    const Track k = make_track(d, tr);
+    if (ldv(d.e + v) * k.sign > 0) activate(d, k, nxt, v, e & TRACK_BIT, sm);
+  }
+  __syncwarp();
+  if (lane == 0) sm.wcc[w] = 0;
+  __syncwarp();
+}
+
+__device__ __forceinline__ void async_phase(const Dev &d, Smem &sm, const BL &init, const int32_t c[NB], const BL &rl,
+                                            const BL &nxt) {
+  const int lane = threadIdx.x & 31;
+  WarpG g{lane};
+  Ctl *ctl = d.ctl;
+  const int32_t c3 = c[3], c31 = c[3] + c[1], total = c[3] + c[1] + c[0];
+  if ((int)(threadIdx.x >> 5) >= d.async_warps) return;   // consumer warps per CTA (fewer pollers)
+  for (;;) {
+    int32_t idx = -1;
+    if (lane == 0 && !async_stopped(d, sm)) idx = atomicAdd(&ctl->ahead, 1);
+    idx = __shfl_sync(0xffffffffu, idx, 0);
+    if (idx < 0) break;
+    long long e = AQ_EMPTY;
+    if (idx < total) {
+      e = idx < c3 ? init.cq[idx] : (long long)(uint32_t)(idx < c31 ? init.bin(1)[idx - c3] : init.bin(0)[idx - c31]);
+    } else if (lane == 0) {
+      long long *slot = d.aq + ((uint32_t)(idx - total) & (uint32_t)d.aq_mask);
+      for (int spin = 0;; spin++) {
+        e = ldvol(slot);
+        if (e != AQ_EMPTY) { *(volatile long long *)slot = AQ_EMPTY; break; }
+        if (async_stopped(d, sm)) break;
+        __nanosleep(spin < 4 ? 128 : 1024);
+      }
+    }
+    e = __shfl_sync(0xffffffffu, e, 0);
+    if (e == AQ_EMPTY) break;
+    if (lane == 0) DBG(d, 203, (int32_t)((uint32_t)e & ~TRACK_BIT), idx, total, (int32_t)(e >> 32));
+    const int32_t v = (int32_t)((uint32_t)e & ~TRACK_BIT);
+    if (d.row[v + 1] - d.row[v] > BIN1_MAX) discharge_chunk(d, sm, e, rl, nxt);
+    else discharge(d, g, sm, (int32_t)(uint32_t)e, rl, nxt, nullptr);
+    async_candidates(d, sm, nxt);
+    if (lane == 0) {
+      const unsigned long long old = atomicAdd(&ctl->aw, ~0ull);        // item done (after its enqueues)
+      bool stop = (uint32_t)old == 1u;                                    // nothing left anywhere
+      if (!stop && sm.work > 32768ull) {                                  // budget: flushed in 32K-slot units
+        const unsigned long long w = atomicExch(&sm.work, 0ull);
+        stop = (long long)(atomicAdd(&ctl->awork, w) + w) > d.work_budget;
+      }
+      if (stop) { if (!ldvol(&ctl->astop)) atomicExch(&ctl->astop, 1); sm.astop = 1; }
+    }
+  }
+}
+
+// A queued item dropped by a budget stop: clear the vertex's queued flag and, for a
+// chunked vertex (some of whose chunks may already have counted themselves), its
+// chunk protocol state -- none of its chunks runs after the phase's barrier.
+__device__ __forceinline__ void async_unqueue(const Dev &d, long long e) {
+  const int32_t v = (int32_t)((uint32_t)e & ~TRACK_BIT);
+  d.inq[v] = 0;
+  if (d.row[v + 1] - d.row[v] > BIN1_MAX) { d.dcnt[v] = 0; d.dmin[v] = DMIN_NONE; }
+}
+
+// After the phase's barrier: clear the inq flags of items a budget stop left queued.
+__device__ __forceinline__ bool async_sweep(const Dev &d, Smem &sm, const BL &init, const int32_t c[NB]) {
+  const long long w = cta_ld(sm, reinterpret_cast<const long long *>(&d.ctl->aw));
+  const int32_t head = cta_ld(sm, &d.ctl->ahead);
+  if ((uint32_t)w == 0) return false;      // terminated normally: every item was consumed
+  const int32_t c3 = c[3], c31 = c[3] + c[1], total = c[3] + c[1] + c[0];
+  const int32_t gt = blockIdx.x * NT + threadIdx.x, nt = gridDim.x * NT;
+  for (int32_t x = min(head, total) + gt; x < total; x += nt) {
+    const long long e = x < c3 ? init.cq[x] : (long long)(uint32_t)(x < c31 ? init.bin(1)[x - c3] : init.bin(0)[x - c31]);
+    async_unqueue(d, e);
+  }
+  const long long tail = (long long)((unsigned long long)w >> 32);
+  const long long cap = (long long)d.aq_mask + 1;
+  for (long long x = gt; x < (tail < cap ? tail : cap); x += nt) {
+    const long long e = d.aq[x];
+    if (e != AQ_EMPTY) { async_unqueue(d, e); d.aq[x] = AQ_EMPTY; }
+  }
+  return true;
+}
+
+// ---------------------------------------------------------------------------
 // Roots of a global relabel.
 enum ResetKind : int { RK_PUSH = 0, RK_PP = 1, RK_STAGE2 = 2, RK_MINCUT = 3, RK_MAXCUT = 4, RK_MINCUT_P = 5 };
 
@@ -1332,6 +1508,7 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
    if (!(warm && iter == 0)) {
     // ---------------- RESET: heights of the domain, roots -> frontier level 0
     if (blockIdx.x == 0 && threadIdx.x < NB) {
+      if (threadIdx.x == 0) { ctl->aw = 0; ctl->ahead = 0; ctl->astop = 0; ctl->awork = 0; }
       rlc[threadIdx.x] = 0;
       qc[NB + threadIdx.x] = 0;
       if (threadIdx.x < 3) ctl->work[threadIdx.x] = 0;
@@ -1466,7 +1643,24 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
     // (Alg.1 l.168-169: PushRelabel, then RemoveInvalidEdges, then the next BFS)
     unsigned long long spent = 0;                 // work since the global relabel (same in every thread)
     const BL rl{L.rl, rlc, n, L.rlc};
-    for (int r = 0;; ++r) {
+    int32_t w_async[NB];
+    if (d.async) cta_counts(sm, wlc, w_async);
+    if (d.async && total(w_async) > 0) {
+      const int32_t *w = w_async;
+      if (lead) ctl->aw = (unsigned long long)total(w);   // (tail 0) published by the barrier below
+      if (threadIdx.x == 0) { sm.astop = 0; sm.apoll = 0; }
+      gsync(d, grid, sm);
+      const BL init{L.wl0, wlc, n, L.cw0};
+      async_phase(d, sm, init, w, rl, BL{L.wl1, wlc + NB, n, L.cw1});
+      dis_flush(d, sm, BL{L.wl1, wlc + NB, n, L.cw1}, rl);
+      if (threadIdx.x == 0 && sm.work) { atomicAdd(&ctl->awork, sm.work); sm.work = 0; }
+      if (lead) sstat_add(sm, ST_ROUNDS, 1);
+      gsync(d, grid, sm);
+      clk.lap(d, sm, ST_T_DIS, iter, 0, total(w), w[3]);
+      const bool stopped = async_sweep(d, sm, init, w);
+      if (lead && stopped) sstat_add(sm, ST_BUDGET_STOPS, 1);
+    }
+    for (int r = 0; !d.async; ++r) {
       // wlc / work rings of 3: round r reads [r%3], fills [(r+1)%3]; a slot is zeroed
       // only when every block has passed the barrier after its last read
       const int cur = r % 3, nx = (r + 1) % 3, nn = (r + 2) % 3;
@@ -1565,7 +1759,8 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(const __grid_con
   __shared__ Smem sm;
   for (int i = threadIdx.x; i < ST_N; i += NTHREADS) sm.stat[i] = 0;
   if (threadIdx.x < 6) sm.st.cnt[threadIdx.x] = 0;
-  if (threadIdx.x == 0) { sm.work = 0; sm.tprev = gtimer(); sm.acnt = 0; sm.rcnt = 0; sm.ccnt = 0; }
+  if (threadIdx.x == 0) { sm.work = 0; sm.tprev = gtimer(); sm.acnt = 0; sm.rcnt = 0; sm.ccnt = 0; sm.astop = 0; sm.apoll = 0; }
+  if (threadIdx.x < WPB) sm.wcc[threadIdx.x] = 0;
   __syncthreads();
   const int32_t n = d.n;
   const int32_t gt = blockIdx.x * NTHREADS + threadIdx.x, nt = gridDim.x * NTHREADS;
@@ -1643,10 +1838,10 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(const __grid_con
         const long long ev = ldv(d.e + x);
         if (p == PART_T) {
           if (ev < 0) d.hp[x] = 0;
-          else if (ev > 0 && ldv(d.hp + x) < n) activate(d, make_track(d, 0), wl0, x, 0u, sm);
+          else if (ev > 0 && ldv(d.hp + x) < n) activate(d, make_track(d, 0), wl0, x, 0u, sm, false);
         } else if (p == PART_S) {
           if (ev > 0) d.hm[x] = 0;
-          else if (ev < 0 && ldv(d.hm + x) < n) activate(d, make_track(d, 1), wl0, x, TRACK_BIT, sm);
+          else if (ev < 0 && ldv(d.hm + x) < n) activate(d, make_track(d, 1), wl0, x, TRACK_BIT, sm, false);
         }
       }
       {
