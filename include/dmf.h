@@ -186,6 +186,15 @@ int dmf_sizes(const dmf_graph *g, int32_t *n, int64_t *S, int64_t *m);
 int dmf_export_state(const dmf_graph *g, int64_t *row_ptr, int32_t *dst, int32_t *rev,
                      int32_t *cap, int32_t *res, int64_t *excess);
 
+/* Copy the engine's labels after the last call (host or device buffers; any may be
+ * NULL): hp/hm int32[n] (h+ / h- heights, in [0, |V|+1]: |V| = unreached by the last
+ * global relabel, |V|+1 = outside the track's region), part uint8[n] (1 = S, 2 = T,
+ * 3 = P of Alg.8), rres int32[S] (the residual mirror rres[i] =
+ * c_f(dst[i], u) of slot i = (u, dst[i]); equal to res[rev[i]] whenever no call is
+ * running).  Inspection / invariant checks only: the labels are not part of the
+ * result. */
+int dmf_export_labels(const dmf_graph *g, int32_t *hp, int32_t *hm, uint8_t *part, int32_t *rres);
+
 /* Free every device array of the handle (NULL is a no-op). */
 void dmf_destroy(dmf_graph *g);
 

@@ -82,6 +82,7 @@ def load_library():
         L.dmf_get_stats.argtypes = [P, ctypes.POINTER(Stats)]
         L.dmf_sizes.argtypes = [P, ctypes.POINTER(I32), ctypes.POINTER(I64), ctypes.POINTER(I64)]
         L.dmf_export_state.argtypes = [P, P, P, P, P, P, P]
+        L.dmf_export_labels.argtypes = [P, P, P, P, P]
         L.dmf_set_trace.argtypes = [P, I32]
         L.dmf_get_trace.argtypes = [P, P, I32, ctypes.POINTER(I32)]
         L.dmf_get_trace_cta.argtypes = [P, P, I32, ctypes.POINTER(I32)]
@@ -89,7 +90,7 @@ def load_library():
         L.dmf_destroy.restype = None
         L.dmf_last_error.restype = ctypes.c_char_p
         for f in ("dmf_create", "dmf_static_solve", "dmf_apply_batch", "dmf_flow_value", "dmf_min_cut_source_side",
-                  "dmf_max_cut_source_side", "dmf_get_stats", "dmf_sizes", "dmf_export_state", "dmf_set_trace",
+                  "dmf_max_cut_source_side", "dmf_get_stats", "dmf_sizes", "dmf_export_state", "dmf_export_labels", "dmf_set_trace",
                   "dmf_get_trace", "dmf_get_trace_cta"):
             getattr(L, f).restype = ctypes.c_int
         _lib = L
@@ -264,6 +265,14 @@ class DynMaxFlow:
         e = np.zeros(self.n, np.int64)
         self._check(self._L.dmf_export_state(self._h, _ptr(row_ptr), _ptr(dst), _ptr(rev), _ptr(cap), _ptr(res), _ptr(e)))
         return dict(row_ptr=row_ptr, dst=dst, rev=rev, cap=cap, res=res, e=e)
+
+    def export_labels(self) -> dict:
+        hp = np.zeros(self.n, np.int32)
+        hm = np.zeros(self.n, np.int32)
+        part = np.zeros(self.n, np.uint8)
+        rres = np.zeros(self.S, np.int32)
+        self._check(self._L.dmf_export_labels(self._h, _ptr(hp), _ptr(hm), _ptr(part), _ptr(rres)))
+        return dict(hp=hp, hm=hm, part=part, rres=rres)
 
     def close(self):
         if getattr(self, "_h", None):

@@ -70,6 +70,7 @@ struct dmf_graph {
   int32_t aq_mask = 0;
   bool async = true;         // DMF_ASYNC=0: barrier-separated discharge rounds
   int32_t async_warps = 8;   // DMF_ASYNC_WARPS
+  long long async_tmax_us = 300;   // DMF_ASYNC_TMAX_US
   long long budget_mul = 1;  // DMF_BUDGET_MUL: discharge work between global relabels, in whole-graph BFS units
   long long *e = nullptr;
   uint8_t *part = nullptr, *mask = nullptr, *rlf = nullptr;
@@ -231,6 +232,7 @@ static Dev make_dev(dmf_graph *g) {
   d.dcnt = g->dcnt; d.dmin = g->dmin;
   d.aq = g->aq; d.aq_mask = g->aq_mask; d.async = g->async ? 1 : 0;
   d.async_warps = g->async_warps;
+  d.async_tmax_ns = g->async_tmax_us * 1000LL;
   d.plist = g->plist; d.stamp = g->stamp;
   d.mask = g->mask; d.ctl = g->ctl;
   d.dbg = g->ddbg;
@@ -464,6 +466,7 @@ int dmf_create(int32_t n, const int64_t *row_ptr, const int32_t *col, const int3
   if (const char *nw = getenv("DMF_NO_WARM")) g->no_warm = atoi(nw) != 0;
   if (const char *as = getenv("DMF_ASYNC")) g->async = atoi(as) != 0;
   if (const char *aw = getenv("DMF_ASYNC_WARPS")) g->async_warps = atoi(aw) > 0 ? (atoi(aw) < WPB ? atoi(aw) : WPB) : 8;
+  if (const char *tm = getenv("DMF_ASYNC_TMAX_US")) g->async_tmax_us = atoll(tm) > 0 ? atoll(tm) : 300;
   if (const char *bm = getenv("DMF_BUDGET_MUL")) g->budget_mul = atoll(bm) > 0 ? atoll(bm) : 1;
   if (const char *wd = getenv("DMF_WATCHDOG_S")) {
     g->watchdog_s = atof(wd);
@@ -660,6 +663,18 @@ int dmf_export_state(const dmf_graph *g, int64_t *row_ptr, int32_t *dst, int32_t
   if (cap) CK(cudaMemcpyAsync(cap, g->cap, g->S * 4, cudaMemcpyDefault, st));
   if (res) CK(cudaMemcpyAsync(res, g->res, g->S * 4, cudaMemcpyDefault, st));
   if (excess) CK(cudaMemcpyAsync(excess, g->e, (size_t)g->n * 8, cudaMemcpyDefault, st));
+  CK(cudaStreamSynchronize(st));
+  return DMF_OK;
+}
+
+int dmf_export_labels(const dmf_graph *g, int32_t *hp, int32_t *hm, uint8_t *part, int32_t *rres) {
+  g_last_error.clear();
+  if (!g) return fail(DMF_EINVAL, "NULL handle");
+  cudaStream_t st = g->stream;
+  if (hp) CK(cudaMemcpyAsync(hp, g->hp, (size_t)g->n * 4, cudaMemcpyDefault, st));
+  if (hm) CK(cudaMemcpyAsync(hm, g->hm, (size_t)g->n * 4, cudaMemcpyDefault, st));
+  if (part) CK(cudaMemcpyAsync(part, g->part, (size_t)g->n, cudaMemcpyDefault, st));
+  if (rres) CK(cudaMemcpyAsync(rres, g->rres, (size_t)g->S * 4, cudaMemcpyDefault, st));
   CK(cudaStreamSynchronize(st));
   return DMF_OK;
 }

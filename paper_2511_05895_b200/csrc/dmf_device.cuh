@@ -109,6 +109,7 @@ struct Dev {
   int32_t aq_mask;
   int32_t async;             // 1: asynchronous discharge phase, 0: barrier-separated rounds
   int32_t async_warps;       // consumer warps per CTA in the asynchronous phase
+  long long async_tmax_ns;   // time budget of one asynchronous phase (then a global relabel)
   int32_t *plist;            // region P of push-pull stage 2
   int32_t *stamp;            // per-slot batch stamp (duplicate detection)
   const int32_t *bu, *bv, *bc;  // batch entries
@@ -146,7 +147,11 @@ __device__ __forceinline__ uint8_t ldv(const uint8_t *p) { return __ldcg(p); }
 // construction).  Safe across phases: the grid barrier's ld.acquire.gpu + CTA
 // barrier (cooperative_groups sync_grids_wait) orders the SM's later weak loads
 // after every write made before the barrier, so no stale L1 line survives it.
+#ifdef DMF_NO_L1
+__device__ __forceinline__ int32_t ldl1(const int32_t *p) { return __ldcg(p); }
+#else
 __device__ __forceinline__ int32_t ldl1(const int32_t *p) { return __ldca(p); }
+#endif
 __device__ __forceinline__ uint32_t ldl1(const uint32_t *p) { return __ldca(p); }
 __device__ __forceinline__ void atom_add(long long *p, long long x) {
   atomicAdd(reinterpret_cast<unsigned long long *>(p), static_cast<unsigned long long>(x));

@@ -66,6 +66,7 @@ struct Smem {
   int32_t wcc[WPB];                // async discharge: per-warp candidate counts (warp w: cand[w*WCAP..])
   int32_t astop;                   // async discharge: this CTA has seen ctl->astop
   unsigned long long apoll;        // async discharge: last global poll of ctl->astop
+  unsigned long long astart;       // async discharge: this CTA's phase start (time budget)
   int32_t cand[2048];
   Stage st;                    // block-staged appends (BFS)
   TileSm ts;                   // tiled compaction (dense top-down BFS levels)
@@ -1419,6 +1420,10 @@ __device__ __forceinline__ void async_phase(const Dev &d, Smem &sm, const BL &in
     if (lane == 0) {
       const unsigned long long old = atomicAdd(&ctl->aw, ~0ull);        // item done (after its enqueues)
       bool stop = (uint32_t)old == 1u;                                    // nothing left anywhere
+      // time budget: a long phase means excess creeping up one lift at a time on stale
+      // heights (a ping-pong the rounds bounded by charging every round); a global
+      // relabel fixes every height at once
+      if (!stop && gtimer() - sm.astart > (unsigned long long)d.async_tmax_ns) stop = true;
       if (!stop && sm.work > 32768ull) {                                  // budget: flushed in 32K-slot units
         const unsigned long long w = atomicExch(&sm.work, 0ull);
         stop = (long long)(atomicAdd(&ctl->awork, w) + w) > d.work_budget;
@@ -1650,6 +1655,8 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
       if (lead) ctl->aw = (unsigned long long)total(w);   // (tail 0) published by the barrier below
       if (threadIdx.x == 0) { sm.astop = 0; sm.apoll = 0; }
       gsync(d, grid, sm);
+      if (threadIdx.x == 0) sm.astart = gtimer();
+      __syncthreads();
       const BL init{L.wl0, wlc, n, L.cw0};
       async_phase(d, sm, init, w, rl, BL{L.wl1, wlc + NB, n, L.cw1});
       dis_flush(d, sm, BL{L.wl1, wlc + NB, n, L.cw1}, rl);
@@ -1890,10 +1897,16 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(const __grid_con
     }
     __syncthreads();
     {
-      const int32_t c = min(sm.acnt, ACAP);
-      if (threadIdx.x == 0) { sm.ts.base[0] = c ? atomicAdd(&ctl->pcnt, c) : 0; sm.acnt = 0; }
+      if (threadIdx.x == 0) {
+        const int32_t c0 = min(sm.acnt, ACAP);
+        sm.ts.cnt[0] = c0;
+        sm.ts.base[0] = c0 ? atomicAdd(&ctl->pcnt, c0) : 0;
+        sm.acnt = 0;
+      }
       __syncthreads();
+      const int32_t c = sm.ts.cnt[0];
       for (int32_t x = threadIdx.x; x < c; x += NTHREADS) d.plist[sm.ts.base[0] + x] = act_buf(sm)[x];
+      __syncthreads();
     }
     gsync(d, grid, sm);
     const int32_t pc = cta_ld(sm, &ctl->pcnt);
