@@ -249,6 +249,7 @@ static int run_solve(dmf_graph *g, int32_t mode, const Dev &dv) {
   g->warm = false;                                  // every launch rewrites hp or hm
   CK(cudaMemsetAsync(g->ctl, 0, sizeof(Ctl), g->stream));
   CK(cudaEventRecord(g->ev0, g->stream));
+  d.async_tmax_any = mode == MODE_STATIC ? 0 : 1;
   int32_t md = mode;
   void *args[] = {&d, &md};
   CK(cudaLaunchCooperativeKernel((const void *)k_solve<NT>, dim3(g->grid_blocks), dim3(NT), args, 0, g->stream));

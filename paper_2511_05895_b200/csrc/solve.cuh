@@ -1423,7 +1423,10 @@ __device__ __forceinline__ void async_phase(const Dev &d, Smem &sm, const BL &in
       // time budget: a long phase means excess creeping up one lift at a time on stale
       // heights (a ping-pong the rounds bounded by charging every round); a global
       // relabel fixes every height at once
-      if (!stop && gtimer() - sm.astart > (unsigned long long)d.async_tmax_ns) stop = true;
+      // (a repair after a batch: always; the static solve from zero flow: only while
+      // little is pending -- a long phase with plenty of parallel work is useful there)
+      if (!stop && (d.async_tmax_any || (uint32_t)old <= 64u) && gtimer() - sm.astart > (unsigned long long)d.async_tmax_ns)
+        stop = true;
       if (!stop && sm.work > 32768ull) {                                  // budget: flushed in 32K-slot units
         const unsigned long long w = atomicExch(&sm.work, 0ull);
         stop = (long long)(atomicAdd(&ctl->awork, w) + w) > d.work_budget;
