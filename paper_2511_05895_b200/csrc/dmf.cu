@@ -68,7 +68,8 @@ struct dmf_graph {
   int32_t *dcnt = nullptr, *dmin = nullptr;
   long long *aq = nullptr;
   int32_t aq_mask = 0;
-  bool async = true;         // DMF_ASYNC=0: barrier-separated discharge rounds
+  bool async = true;         // repairs (DYN_PR / DYN_PP): asynchronous discharge; DMF_ASYNC=0: rounds
+  bool async_static = false; // static solve from zero flow: rounds (massively parallel work); DMF_ASYNC_STATIC=1: async
   int32_t async_warps = 8;   // DMF_ASYNC_WARPS
   long long async_tmax_us = 300;   // DMF_ASYNC_TMAX_US
   long long budget_mul = 1;  // DMF_BUDGET_MUL: discharge work between global relabels, in whole-graph BFS units
@@ -250,6 +251,7 @@ static int run_solve(dmf_graph *g, int32_t mode, const Dev &dv) {
   CK(cudaMemsetAsync(g->ctl, 0, sizeof(Ctl), g->stream));
   CK(cudaEventRecord(g->ev0, g->stream));
   d.async_tmax_any = mode == MODE_STATIC ? 0 : 1;
+  d.async = (mode == MODE_STATIC ? g->async_static : g->async) ? 1 : 0;
   int32_t md = mode;
   void *args[] = {&d, &md};
   CK(cudaLaunchCooperativeKernel((const void *)k_solve<NT>, dim3(g->grid_blocks), dim3(NT), args, 0, g->stream));
@@ -466,6 +468,7 @@ int dmf_create(int32_t n, const int64_t *row_ptr, const int32_t *col, const int3
   CKB(cudaMallocHost((void **)&g->hctl, sizeof(Ctl)));
   if (const char *nw = getenv("DMF_NO_WARM")) g->no_warm = atoi(nw) != 0;
   if (const char *as = getenv("DMF_ASYNC")) g->async = atoi(as) != 0;
+  if (const char *ss = getenv("DMF_ASYNC_STATIC")) g->async_static = atoi(ss) != 0;
   if (const char *aw = getenv("DMF_ASYNC_WARPS")) g->async_warps = atoi(aw) > 0 ? (atoi(aw) < WPB ? atoi(aw) : WPB) : 8;
   if (const char *tm = getenv("DMF_ASYNC_TMAX_US")) g->async_tmax_us = atoll(tm) > 0 ? atoll(tm) : 300;
   if (const char *bm = getenv("DMF_BUDGET_MUL")) g->budget_mul = atoll(bm) > 0 ? atoll(bm) : 1;
