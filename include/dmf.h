@@ -186,6 +186,23 @@ int dmf_sizes(const dmf_graph *g, int32_t *n, int64_t *S, int64_t *m);
 int dmf_export_state(const dmf_graph *g, int64_t *row_ptr, int32_t *dst, int32_t *rev,
                      int32_t *cap, int32_t *res, int64_t *excess);
 
+/* Stage (ii): turn the converged pseudoflow
+ * into a true maximum flow in place.  Stuck excess is returned to s (every vertex with
+ * excess reaches s in the residual graph, Lemma 4) and every deficit is
+ * filled from t, with the same device engine (roots {s}, then {t}).  F,
+ * S_min and S_max are unchanged; afterwards e(v) = 0 for every v not in {s,t} and
+ * e(t) = -e(s) = F.  The next DYN_PP call starts with a full global relabel (the warm
+ * labels are gone).  DMF_ESTATE before any solve; DMF_ENOCONV if a vertex keeps
+ * excess or deficit (not expected: the lemmas guarantee the paths). */
+int dmf_to_flow(dmf_graph *g);
+
+/* Per-slot flow of the current state: flow[i] = max(0, cap[i] - res[i]) for slot i =
+ * (u, dst[i]) (the net flow of the pair {u, dst[i]} in that direction; the reverse
+ * slot holds the other direction, so at most one of the two is positive).  After
+ * dmf_to_flow this is a feasible maximum flow.  flow: int32[S], host or device,
+ * slot order of dmf_export_state. */
+int dmf_edge_flow(dmf_graph *g, int32_t *flow);
+
 /* Copy the engine's labels after the last call (host or device buffers; any may be
  * NULL): hp/hm int32[n] (h+ / h- heights, in [0, |V|+1]: |V| = unreached by the last
  * global relabel, |V|+1 = outside the track's region), part uint8[n] (1 = S, 2 = T,

@@ -83,6 +83,8 @@ def load_library():
         L.dmf_sizes.argtypes = [P, ctypes.POINTER(I32), ctypes.POINTER(I64), ctypes.POINTER(I64)]
         L.dmf_export_state.argtypes = [P, P, P, P, P, P, P]
         L.dmf_export_labels.argtypes = [P, P, P, P, P]
+        L.dmf_to_flow.argtypes = [P]
+        L.dmf_edge_flow.argtypes = [P, P]
         L.dmf_set_trace.argtypes = [P, I32]
         L.dmf_get_trace.argtypes = [P, P, I32, ctypes.POINTER(I32)]
         L.dmf_get_trace_cta.argtypes = [P, P, I32, ctypes.POINTER(I32)]
@@ -90,7 +92,7 @@ def load_library():
         L.dmf_destroy.restype = None
         L.dmf_last_error.restype = ctypes.c_char_p
         for f in ("dmf_create", "dmf_static_solve", "dmf_apply_batch", "dmf_flow_value", "dmf_min_cut_source_side",
-                  "dmf_max_cut_source_side", "dmf_get_stats", "dmf_sizes", "dmf_export_state", "dmf_export_labels", "dmf_set_trace",
+                  "dmf_max_cut_source_side", "dmf_get_stats", "dmf_sizes", "dmf_export_state", "dmf_export_labels", "dmf_to_flow", "dmf_edge_flow", "dmf_set_trace",
                   "dmf_get_trace", "dmf_get_trace_cta"):
             getattr(L, f).restype = ctypes.c_int
         _lib = L
@@ -265,6 +267,17 @@ class DynMaxFlow:
         e = np.zeros(self.n, np.int64)
         self._check(self._L.dmf_export_state(self._h, _ptr(row_ptr), _ptr(dst), _ptr(rev), _ptr(cap), _ptr(res), _ptr(e)))
         return dict(row_ptr=row_ptr, dst=dst, rev=rev, cap=cap, res=res, e=e)
+
+    def to_flow(self) -> int:
+        """Stage (ii): convert the state into a true maximum flow (dmf_to_flow); returns F."""
+        self._check(self._L.dmf_to_flow(self._h))
+        return self.flow_value()
+
+    def edge_flow(self, out=None):
+        """Per-slot flow max(0, cap - res), int32[S] in dmf_export_state's slot order."""
+        out = np.zeros(self.S, np.int32) if out is None else out
+        self._check(self._L.dmf_edge_flow(self._h, _ptr(out)))
+        return out
 
     def export_labels(self) -> dict:
         hp = np.zeros(self.n, np.int32)

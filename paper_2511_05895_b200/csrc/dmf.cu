@@ -245,6 +245,7 @@ static Dev make_dev(dmf_graph *g) {
 
 static int run_solve(dmf_graph *g, int32_t mode, const Dev &dv) {
   Dev d = dv;
+  const bool smin_before = g->smin_valid;
   if (mode != MODE_MINCUT) g->smin_valid = false;  // the state (or the mask buffer) is about to change
   const bool warm_before = g->warm;
   g->warm = false;                                  // every launch rewrites hp or hm
@@ -314,11 +315,15 @@ static int run_solve(dmf_graph *g, int32_t mode, const Dev &dv) {
     if (c.status != DMF_ENOCONV) g->warm = warm_before;   // rejected before any mutation
     return fail(c.status, "%s (batch entry %d)", what, c.err_entry);
   }
+  if (mode == MODE_FLOW && c.flow != g->flow)
+    return fail(DMF_ENOCONV, "stage (ii) changed F (%lld -> %lld)", (long long)g->flow, (long long)c.flow);
   if (mode == MODE_STATIC || mode == MODE_PR || mode == MODE_PP) {
     g->flow = c.flow;
     g->solved = true;
   }
-  g->smin_valid = mode == MODE_PP || mode == MODE_MINCUT;   // MAXCUT / STATIC / PR leave no S_min
+  // MAXCUT / STATIC / PR leave no S_min; FLOW keeps it (stage (ii) moves flow only
+  // inside S_max and inside T, and S_min of a maximum flow is unique)
+  g->smin_valid = mode == MODE_PP || mode == MODE_MINCUT || (mode == MODE_FLOW && smin_before);
   g->warm = mode == MODE_PP && !g->no_warm;
   return DMF_OK;
 }
@@ -594,6 +599,46 @@ static int cut_query(dmf_graph *g, uint8_t *mask, int32_t mode) {
 }
 
 int dmf_min_cut_source_side(dmf_graph *g, uint8_t *mask) { return cut_query(g, mask, MODE_MINCUT); }
+
+int dmf_to_flow(dmf_graph *g) {
+  g_last_error.clear();
+  if (!g) return fail(DMF_EINVAL, "NULL handle");
+  if (!g->solved) return fail(DMF_ESTATE, "no converged solve yet");
+  dmf_stats keep = g->stats;
+  Dev d = make_dev(g);
+  const int rc = run_solve(g, MODE_FLOW, d);
+  g->stats = keep;
+  return rc;
+}
+
+namespace {
+__global__ void k_edge_flow(int64_t S, const int32_t *cap, const int32_t *res, int32_t *out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < S; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t x = cap[i] - res[i];      // net flow on the pair, seen from this slot
+    out[i] = x > 0 ? x : 0;
+  }
+}
+}  // namespace
+
+int dmf_edge_flow(dmf_graph *g, int32_t *flow) {
+  g_last_error.clear();
+  if (!g || !flow) return fail(DMF_EINVAL, "NULL argument");
+  if (!g->solved) return fail(DMF_ESTATE, "no converged solve yet");
+  int32_t *dst = flow;
+  const bool dev = is_device_ptr(flow);
+  if (!dev) {
+    dst = (int32_t *)g->alloc((size_t)g->S * 4);
+    if (!dst) return fail(DMF_ENOMEM, "device allocation failed (edge flow)");
+  }
+  if (g->S) k_edge_flow<<<(int)(g->S < 148LL * 256 * 16 ? (g->S + 255) / 256 : 148LL * 16), 256, 0, g->stream>>>(g->S, g->cap, g->res, dst);
+  g->launches++;
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess && !dev) e = cudaMemcpyAsync(flow, dst, (size_t)g->S * 4, cudaMemcpyDeviceToHost, g->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+  if (!dev) g->release(dst);
+  if (e != cudaSuccess) return fail(DMF_ECUDA, "edge flow: %s", cudaGetErrorString(e));
+  return DMF_OK;
+}
 int dmf_max_cut_source_side(dmf_graph *g, uint8_t *mask) { return cut_query(g, mask, MODE_MAXCUT); }
 
 int dmf_set_trace(dmf_graph *g, int32_t capacity) {

@@ -40,6 +40,7 @@ enum Mode : int32_t {
   MODE_PP = 2,       // batch + Alg.8
   MODE_MINCUT = 3,   // forward reach of {s} u Exc  (S_min)
   MODE_MAXCUT = 4,   // complement of backward reach of {t} u Def (S_max)
+  MODE_FLOW = 5,     // stage (ii): pseudoflow -> true maximum flow (excess back to s, deficits from t)
 };
 
 enum Stat : int {

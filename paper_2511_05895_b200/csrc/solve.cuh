@@ -1467,7 +1467,9 @@ __device__ __forceinline__ bool async_sweep(const Dev &d, Smem &sm, const BL &in
 
 // ---------------------------------------------------------------------------
 // Roots of a global relabel.
-enum ResetKind : int { RK_PUSH = 0, RK_PP = 1, RK_STAGE2 = 2, RK_MINCUT = 3, RK_MAXCUT = 4, RK_MINCUT_P = 5 };
+enum ResetKind : int { RK_PUSH = 0, RK_PP = 1, RK_STAGE2 = 2, RK_MINCUT = 3, RK_MAXCUT = 4, RK_MINCUT_P = 5,
+                       RK_RETURN_S = 6,   // stage (ii): push track, roots {s}: excess flows back to s (Lemma 4)
+                       RK_FILL_T = 7 };   // stage (ii): pull track, roots {t}: deficits are filled from t
 
 struct Lists {      // (members, not arrays: a dynamically indexed array would live in local memory)
   int32_t *q0, *q1;       // frontier ping-pong, [NB bins][n] each
@@ -1505,8 +1507,8 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
   Ctl *ctl = d.ctl;
   int32_t *qc = ctl->qc, *wlc = ctl->wlc, *rlc = ctl->rlc;
   const int32_t nt = gridDim.x * NT;
-  const bool use0 = kind != RK_MINCUT && kind != RK_MINCUT_P;
-  const bool use1 = kind == RK_PP || kind == RK_MINCUT || kind == RK_MINCUT_P;
+  const bool use0 = kind != RK_MINCUT && kind != RK_MINCUT_P && kind != RK_FILL_T;
+  const bool use1 = kind == RK_PP || kind == RK_MINCUT || kind == RK_MINCUT_P || kind == RK_FILL_T;
   const bool on_plist = kind == RK_STAGE2 || kind == RK_MINCUT_P;
   const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
   for (int iter = 0;; ++iter) {
@@ -1552,6 +1554,14 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
             r0 = ev < 0;                        // belong to T\P, which no P vertex reaches
             in0 = true;
             d.hp[v] = r0 ? 0 : n;
+          } else if (kind == RK_RETURN_S) {     // t is outside the region: its excess is F
+            r0 = v == d.s;
+            in0 = v != d.t;
+            d.hp[v] = r0 ? 0 : (in0 ? n : n + 1);
+          } else if (kind == RK_FILL_T) {       // s is outside the region
+            r1 = v == d.t;
+            in1 = v != d.s;
+            d.hm[v] = r1 ? 0 : (in1 ? n : n + 1);
           } else if (kind == RK_MINCUT_P) {     // forward reach of the excess left in P
             r1 = ev > 0;
             in1 = true;
@@ -1940,6 +1950,27 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(const __grid_con
       const long long ev = ldv(d.e + v);
       f += v == d.t ? ev : (v != d.s && ev < 0 ? ev : 0);
       d.mask[v] = ldv(d.hm + v) < n ? 1 : 0;     // S_min, cached for dmf_min_cut_source_side
+    }
+    f = bg.sum(f);
+    if (threadIdx.x == 0 && f) atomicAdd(reinterpret_cast<unsigned long long *>(&ctl->flow), (unsigned long long)f);
+  } else if (mode == MODE_FLOW) {
+    // Stage (ii): turn the converged pseudoflow into a
+    // true maximum flow.  Every vertex with excess reaches s in the residual graph
+    // (Lemma 4) and every deficient vertex is reached from t;
+    // neither can reach the other side at convergence, so F is unchanged.  The same
+    // engine runs twice: push track with roots {s}, then pull track with roots {t}.
+    device_loop(d, grid, sm, clk, RK_RETURN_S, true, false);
+    if (blockIdx.x == 0 && threadIdx.x < NB) {
+      ctl->qc[threadIdx.x] = 0;
+      if (threadIdx.x < 2) { ctl->fs[threadIdx.x] = 0; ctl->mu[threadIdx.x] = 0; }
+    }
+    gsync(d, grid, sm);
+    device_loop(d, grid, sm, clk, RK_FILL_T, true, false);
+    long long f = 0;
+    for (int32_t v = gt; v < n; v += nt) {
+      const long long ev = ldv(d.e + v);
+      f += v == d.t ? ev : (v != d.s && ev < 0 ? ev : 0);
+      if (v != d.s && v != d.t && ev != 0) set_status(d, -8, v);   // not a flow: DMF_ENOCONV
     }
     f = bg.sum(f);
     if (threadIdx.x == 0 && f) atomicAdd(reinterpret_cast<unsigned long long *>(&ctl->flow), (unsigned long long)f);

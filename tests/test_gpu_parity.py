@@ -257,6 +257,66 @@ def test_static_resolve_after_batches_matches(dmf):
         assert np.array_equal(f.min_cut_source_side(), mask_d)
 
 
+# ------------------------------------------------------------------ stage (ii): true flow
+
+def _assert_true_flow(f, g, F, tag):
+    """The exported state is a feasible maximum flow of value F: e(v) = 0 off {s,t},
+    e(t) = -e(s) = F, 0 <= res <= cap + cap_rev, net outflow of every vertex = -e(v)
+    (conservation), and dmf_edge_flow = max(0, cap - res) within [0, cap]."""
+    st = f.export_state()
+    e, rp, res, cap, rev = st["e"], st["row_ptr"], st["res"], st["cap"], st["rev"]
+    off = np.ones(g.n, bool); off[[g.s, g.t]] = False
+    assert not e[off].any(), f"{tag}: {int((e[off] != 0).sum())} vertices keep excess/deficit"
+    assert e[g.t] == F and e[g.s] == -F, f"{tag}: e(t)={e[g.t]} e(s)={e[g.s]} F={F}"
+    assert (res >= 0).all() and (res <= cap.astype(np.int64) + cap[rev]).all(), f"{tag}: capacity"
+    src = np.repeat(np.arange(g.n), np.diff(rp))
+    net = np.bincount(src, weights=(cap.astype(np.int64) - res), minlength=g.n)
+    assert np.array_equal(net.astype(np.int64), -e), f"{tag}: conservation"
+    fl = f.edge_flow()
+    assert np.array_equal(fl, np.maximum(cap - res, 0)) and (fl <= cap).all(), f"{tag}: edge flow"
+    assert not ((fl > 0) & (fl[rev] > 0)).any(), f"{tag}: both directions of a pair carry flow"
+
+
+@pytest.mark.parametrize("algo", ["pr", "pp"])
+def test_to_flow_clrs_chain(dmf, algo):
+    """dmf_to_flow after every CLRS batch (decrements below the flow leave deficits
+    that must be filled from t): a true flow, F / S_min unchanged, later batches exact."""
+    d = load("clrs_26_1.txt")
+    g = graph(d)
+    f = dmf.DynMaxFlow.from_graph(g)
+    f.static_solve()
+    st = W.CapState(g)
+    for j, step in enumerate(d["steps"]):
+        bb = W.as_batch(step["batch"])
+        st.apply(bb)
+        f.apply_batch(bb.u, bb.v, bb.new_cap, algo=algo)
+        F, smin = f.flow_value(), f.min_cut_source_side()
+        assert f.to_flow() == F == step["F"]
+        assert np.array_equal(f.min_cut_source_side(), smin)
+        _assert_true_flow(f, st.graph(), F, f"clrs b{j} {algo}")
+    f.close()
+
+
+@pytest.mark.parametrize("scale,algo", [(12, "pp"), (14, "pr"), (14, "pp")])
+def test_to_flow_rmat(dmf, scale, algo):
+    """Stage (ii) on RMAT after static + mixed batches, then more batches on the
+    converted state: F, S_min and S_max stay bit-exact with the oracle."""
+    g = W.rmat(scale, 16, 1, 7)
+    f = dmf.DynMaxFlow.from_graph(g)
+    f.static_solve()
+    st = W.CapState(g)
+    for j in range(4):
+        b = W.rmat_batch(g, st, 0.01, 900 + j)
+        st.apply(b)
+        f.apply_batch(b.u, b.v, b.new_cap, algo=algo)
+        if j % 2 == 0:
+            F = f.flow_value()
+            assert f.to_flow() == F
+            _assert_true_flow(f, st.graph(), F, f"rmat{scale} b{j} {algo}")
+        _verify(f, st.graph(), f"rmat{scale} b{j} {algo} (after stage ii)")
+    f.close()
+
+
 # ------------------------------------------------------------------ full-size configs
 # BASELINE.json configs 2-5 at full size, in the launch configuration bench.py times
 # (default grid, KERNELCYCLES = floor(m/n)).  F and S_min are compared bit-exactly
