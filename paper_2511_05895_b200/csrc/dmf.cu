@@ -71,6 +71,7 @@ struct dmf_graph {
   bool async = true;         // repairs (DYN_PR / DYN_PP): asynchronous discharge; DMF_ASYNC=0: rounds
   bool async_static = false; // static solve from zero flow: rounds (massively parallel work); DMF_ASYNC_STATIC=1: async
   int32_t async_warps = 8;   // DMF_ASYNC_WARPS
+  int32_t async_sleep_ns = 1024;   // DMF_ASYNC_SLEEP_NS
   long long async_tmax_us = 300;   // DMF_ASYNC_TMAX_US
   long long budget_mul = 1;  // DMF_BUDGET_MUL: discharge work between global relabels, in whole-graph BFS units
   long long *e = nullptr;
@@ -233,6 +234,7 @@ static Dev make_dev(dmf_graph *g) {
   d.dcnt = g->dcnt; d.dmin = g->dmin;
   d.aq = g->aq; d.aq_mask = g->aq_mask; d.async = g->async ? 1 : 0;
   d.async_warps = g->async_warps;
+  d.async_sleep_ns = g->async_sleep_ns;
   d.async_tmax_ns = g->async_tmax_us * 1000LL;
   d.plist = g->plist; d.stamp = g->stamp;
   d.mask = g->mask; d.ctl = g->ctl;
@@ -475,6 +477,7 @@ int dmf_create(int32_t n, const int64_t *row_ptr, const int32_t *col, const int3
   if (const char *as = getenv("DMF_ASYNC")) g->async = atoi(as) != 0;
   if (const char *ss = getenv("DMF_ASYNC_STATIC")) g->async_static = atoi(ss) != 0;
   if (const char *aw = getenv("DMF_ASYNC_WARPS")) g->async_warps = atoi(aw) > 0 ? (atoi(aw) < WPB ? atoi(aw) : WPB) : 8;
+  if (const char *sl = getenv("DMF_ASYNC_SLEEP_NS")) g->async_sleep_ns = atoi(sl) > 0 ? atoi(sl) : 1024;
   if (const char *tm = getenv("DMF_ASYNC_TMAX_US")) g->async_tmax_us = atoll(tm) > 0 ? atoll(tm) : 300;
   if (const char *bm = getenv("DMF_BUDGET_MUL")) g->budget_mul = atoll(bm) > 0 ? atoll(bm) : 1;
   if (const char *wd = getenv("DMF_WATCHDOG_S")) {

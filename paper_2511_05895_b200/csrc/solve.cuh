@@ -1407,7 +1407,7 @@ __device__ __forceinline__ void async_phase(const Dev &d, Smem &sm, const BL &in
         e = ldvol(slot);
         if (e != AQ_EMPTY) { *(volatile long long *)slot = AQ_EMPTY; break; }
         if (async_stopped(d, sm)) break;
-        __nanosleep(spin < 4 ? 128 : 1024);
+        __nanosleep(spin < 4 ? 64 : d.async_sleep_ns);
       }
     }
     e = __shfl_sync(0xffffffffu, e, 0);
@@ -1815,6 +1815,12 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(const __grid_con
     // all updates are commutative atomics.  DYN_PP also saturates a touched S->T slot
     // here (Alg.8 l.10-13, R12): at a converged cut a T->S slot can never go negative,
     // so nothing else changes such a slot in this phase.
+    // e(s) / e(t) deltas are summed per CTA: batches are biased toward s-out and t-in
+    // slots (R20), so per-entry atomics would serialise on those two addresses
+    long long ds = 0, dt = 0;
+    auto eadd = [&](int32_t x, long long delta) {
+      if (x == d.s) ds += delta; else if (x == d.t) dt += delta; else atom_add(d.e + x, delta);
+    };
     for (int64_t j = gt; mode >= 0 && j < d.k; j += nt) {
       const int32_t i = d.bslot[j];
       const int32_t ri = d.rev[i];
@@ -1829,8 +1835,8 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(const __grid_con
         atomicAdd(d.rres + ri, dd);
         atomicAdd(d.res + ri, -dd);
         atomicAdd(d.rres + i, -dd);
-        atom_add(d.e + u, (long long)dd);
-        atom_add(d.e + v, -(long long)dd);
+        eadd(u, (long long)dd);
+        eadd(v, -(long long)dd);
         r = 0;
       }
       if (mode == MODE_PP && r > 0 && d.part[u] == PART_S && d.part[v] == PART_T) {
@@ -1838,11 +1844,17 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(const __grid_con
         atomicAdd(d.rres + ri, -r);
         atomicAdd(d.res + ri, r);
         atomicAdd(d.rres + i, r);
-        atom_add(d.e + v, (long long)r);
-        atom_add(d.e + u, -(long long)r);
+        eadd(v, (long long)r);
+        eadd(u, -(long long)r);
       }
     }
     if (mode >= 0) {
+      ds = bg.sum(ds);
+      dt = bg.sum(dt);
+      if (threadIdx.x == 0) {
+        if (ds) atom_add(d.e + d.s, ds);
+        if (dt) atom_add(d.e + d.t, dt);
+      }
       gsync(d, grid, sm);
       clk.lap(d, sm, ST_T_PRO, 0, 2, (int32_t)d.k);
     }
