@@ -127,6 +127,14 @@ int dmf_create(int32_t n, const int64_t *row_ptr, const int32_t *col, const int3
  * (readings R1, R2, R9 of DESIGN.md: the sink set is {t} u deficient vertices). */
 int dmf_static_solve(dmf_graph *g);
 
+/* Static push-pull variant: as dmf_static_solve, but the
+ * initial preflow also saturates every in-edge (v,t) of the sink, so the tails start
+ * deficient and act as secondary sinks (roots of every global relabel, reading R2)
+ * while the excess from s is pushed into them.  Same F, S_min, S_max and converged
+ * state semantics as dmf_static_solve (F by reading R8); a following DYN_PP batch
+ * starts from its final partition. */
+int dmf_static_solve_pp(dmf_graph *g);
+
 /* Apply a batch of k capacity updates (SET semantics, all entries simultaneous,
  * P:342 "each batch is a set of edges whose new capacities may be either higher or
  * lower") and repair the state to convergence with `algo` (DMF_DYN_PR = Alg.4,

@@ -84,6 +84,7 @@ def load_library():
         L.dmf_export_state.argtypes = [P, P, P, P, P, P, P]
         L.dmf_export_labels.argtypes = [P, P, P, P, P]
         L.dmf_to_flow.argtypes = [P]
+        L.dmf_static_solve_pp.argtypes = [P]
         L.dmf_edge_flow.argtypes = [P, P]
         L.dmf_set_trace.argtypes = [P, I32]
         L.dmf_get_trace.argtypes = [P, P, I32, ctypes.POINTER(I32)]
@@ -91,7 +92,7 @@ def load_library():
         L.dmf_destroy.argtypes = [P]
         L.dmf_destroy.restype = None
         L.dmf_last_error.restype = ctypes.c_char_p
-        for f in ("dmf_create", "dmf_static_solve", "dmf_apply_batch", "dmf_flow_value", "dmf_min_cut_source_side",
+        for f in ("dmf_create", "dmf_static_solve", "dmf_static_solve_pp", "dmf_apply_batch", "dmf_flow_value", "dmf_min_cut_source_side",
                   "dmf_max_cut_source_side", "dmf_get_stats", "dmf_sizes", "dmf_export_state", "dmf_export_labels", "dmf_to_flow", "dmf_edge_flow", "dmf_set_trace",
                   "dmf_get_trace", "dmf_get_trace_cta"):
             getattr(L, f).restype = ctypes.c_int
@@ -190,6 +191,11 @@ class DynMaxFlow:
 
     def static_solve(self) -> int:
         self._check(self._L.dmf_static_solve(self._h))
+        return self.flow_value()
+
+    def static_solve_pp(self) -> int:
+        """Static push-pull solve: t's in-edges saturated too; returns F."""
+        self._check(self._L.dmf_static_solve_pp(self._h))
         return self.flow_value()
 
     def apply_batch(self, u, v, new_cap, algo=None) -> int:

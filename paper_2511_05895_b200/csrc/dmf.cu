@@ -541,6 +541,14 @@ int dmf_static_solve(dmf_graph *g) {
   return run_solve(g, MODE_STATIC, d);
 }
 
+int dmf_static_solve_pp(dmf_graph *g) {
+  g_last_error.clear();
+  if (!g) return fail(DMF_EINVAL, "NULL handle");
+  Dev d = make_dev(g);
+  d.static_pp = 1;
+  return run_solve(g, MODE_STATIC, d);
+}
+
 int dmf_apply_batch(dmf_graph *g, int64_t k, const int32_t *u, const int32_t *v, const int32_t *new_cap, int32_t algo) {
   g_last_error.clear();
   if (!g) return fail(DMF_EINVAL, "NULL handle");

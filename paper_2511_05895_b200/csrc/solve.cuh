@@ -1891,6 +1891,26 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(const __grid_con
     for (int32_t i = beg + gt; i < end; i += nt) tot += saturate_slot(d, i);
     tot = bg.sum(tot);
     if (threadIdx.x == 0 && tot) atom_add(d.e + d.s, -tot);
+    if (mode == MODE_STATIC && d.static_pp) {
+      // static push-pull: also saturate every residual in-edge (v,t); the
+      // deficient tails are secondary sinks -- roots of the global relabel (R2)
+      const int32_t tb = d.row[d.t], te = d.row[d.t + 1];
+      long long into = 0;
+      for (int32_t i = tb + gt; i < te; i += nt) {     // slot i = (t,v), rev[i] = (v,t)
+        if (d.dst[i] == d.s) continue;                 // (s,t) was saturated with s's row
+        const int32_t j = d.rev[i];
+        const int32_t r = ldv(d.res + j);
+        if (r <= 0) continue;
+        d.res[j] = 0;
+        d.rres[i] = 0;
+        atomicAdd(d.res + i, r);
+        atomicAdd(d.rres + j, r);
+        atom_add(d.e + d.dst[i], -(long long)r);
+        into += r;
+      }
+      into = bg.sum(into);
+      if (threadIdx.x == 0 && into) atom_add(d.e + d.t, into);
+    }
     gsync(d, grid, sm);
     clk.lap(d, sm, ST_T_PRO);
     device_loop(d, grid, sm, clk, RK_PUSH, true, false);

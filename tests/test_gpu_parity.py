@@ -257,6 +257,47 @@ def test_static_resolve_after_batches_matches(dmf):
         assert np.array_equal(f.min_cut_source_side(), mask_d)
 
 
+# ------------------------------------------------------------------ static push-pull
+
+def test_static_pp_tiny_random(dmf):
+    """dmf_static_solve_pp on 200 random graphs (n <= 12) vs brute force,
+    then one mixed PP batch each."""
+    for seed in range(200):
+        g = W.tiny_random(seed)
+        f = dmf.DynMaxFlow.from_graph(g)
+        f.static_solve_pp()
+        _verify(f, g, f"tiny{seed} static-pp", small=True)
+        st = W.CapState(g)
+        for j, b in enumerate(W.tiny_batches(g, seed, nb=2)):
+            st.apply(b)
+            f.apply_batch(b.u, b.v, b.new_cap, algo="pp")
+            _verify(f, st.graph(), f"tiny{seed} pp b{j} after static-pp", small=True)
+        f.close()
+
+
+@pytest.mark.parametrize("name", ["clrs", "rmat13", "grid"])
+def test_static_pp_matches(dmf, name):
+    """Static push-pull gives the static solve's F / S_min / S_max (and passes the
+    checker); PP batches continue exactly from its partition."""
+    if name == "clrs":
+        g = graph(load("clrs_26_1.txt"))
+    elif name == "rmat13":
+        g = W.rmat(13, 16, 1, 7)
+    else:
+        g = W.grid(96, 3)
+    f = dmf.DynMaxFlow.from_graph(g)
+    f.static_solve_pp()
+    _verify(f, g, f"{name} static-pp", small=(name == "clrs"))
+    if name == "rmat13":
+        st = W.CapState(g)
+        for j in range(2):
+            b = W.rmat_batch(g, st, 0.01, 950 + j)
+            st.apply(b)
+            f.apply_batch(b.u, b.v, b.new_cap, algo="pp")
+            _verify(f, st.graph(), f"{name} pp b{j} after static-pp")
+    f.close()
+
+
 # ------------------------------------------------------------------ stage (ii): true flow (SURVEY N3)
 
 def _assert_true_flow(f, g, F, tag):
