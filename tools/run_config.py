@@ -27,6 +27,7 @@ def check(gg, F):
     t = time.time(); r = O.maxflow(gg, "fifo_pr"); to = time.time() - t
     m = f.min_cut_source_side()
     print(f"    oracle F={r['F']} ({to:.1f}s) F_ok={r['F'] == F} smin_ok={np.array_equal(m, r['smin'])}", flush=True)
+F = f.static_solve_pp(); show("static-pp", F)
 F = f.static_solve(); show("static", F); check(g, F)
 st = W.CapState(g)
 for j in range(nb):
@@ -39,3 +40,5 @@ for j in range(nb):
     st.apply(b)
     F = f.apply_batch(b.u, b.v, b.new_cap, algo=algo); show(f"{algo} b{j} k={b.k}", F); check(st.graph(), F)
 F = f.static_solve(); show("re-static", F)
+F = f.static_solve_pp(); show("re-static-pp", F)
+F = f.to_flow(); show("to_flow", F)
