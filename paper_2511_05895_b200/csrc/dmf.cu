@@ -71,6 +71,7 @@ struct dmf_graph {
   bool async = true;         // repairs (DYN_PR / DYN_PP): asynchronous discharge; DMF_ASYNC=0: rounds
   bool async_static = false; // static solve from zero flow: rounds (massively parallel work); DMF_ASYNC_STATIC=1: async
   int32_t async_warps = 8;   // DMF_ASYNC_WARPS
+  int32_t bu_alpha = (int32_t)BU_ALPHA, dense_div = (int32_t)DENSE_DIV;   // DMF_BU_ALPHA, DMF_DENSE_DIV
   int32_t async_sleep_ns = 1024;   // DMF_ASYNC_SLEEP_NS
   long long async_tmax_us = 300;   // DMF_ASYNC_TMAX_US
   long long budget_mul = 1;  // DMF_BUDGET_MUL: discharge work between global relabels, in whole-graph BFS units
@@ -234,6 +235,7 @@ static Dev make_dev(dmf_graph *g) {
   d.dcnt = g->dcnt; d.dmin = g->dmin;
   d.aq = g->aq; d.aq_mask = g->aq_mask; d.async = g->async ? 1 : 0;
   d.async_warps = g->async_warps;
+  d.bu_alpha = g->bu_alpha; d.dense_div = g->dense_div;
   d.async_sleep_ns = g->async_sleep_ns;
   d.async_tmax_ns = g->async_tmax_us * 1000LL;
   d.plist = g->plist; d.stamp = g->stamp;
@@ -477,6 +479,8 @@ int dmf_create(int32_t n, const int64_t *row_ptr, const int32_t *col, const int3
   if (const char *as = getenv("DMF_ASYNC")) g->async = atoi(as) != 0;
   if (const char *ss = getenv("DMF_ASYNC_STATIC")) g->async_static = atoi(ss) != 0;
   if (const char *aw = getenv("DMF_ASYNC_WARPS")) g->async_warps = atoi(aw) > 0 ? (atoi(aw) < WPB ? atoi(aw) : WPB) : 8;
+  if (const char *ba = getenv("DMF_BU_ALPHA")) g->bu_alpha = atoi(ba) > 0 ? atoi(ba) : g->bu_alpha;
+  if (const char *dd = getenv("DMF_DENSE_DIV")) g->dense_div = atoi(dd) > 0 ? atoi(dd) : g->dense_div;
   if (const char *sl = getenv("DMF_ASYNC_SLEEP_NS")) g->async_sleep_ns = atoi(sl) > 0 ? atoi(sl) : 1024;
   if (const char *tm = getenv("DMF_ASYNC_TMAX_US")) g->async_tmax_us = atoll(tm) > 0 ? atoll(tm) : 300;
   if (const char *bm = getenv("DMF_BUDGET_MUL")) g->budget_mul = atoll(bm) > 0 ? atoll(bm) : 1;

@@ -112,6 +112,8 @@ struct Dev {
   int32_t async_warps;       // consumer warps per CTA in the asynchronous phase
   long long async_tmax_ns;   // time budget of one asynchronous phase (then a global relabel)
   int32_t static_pp;         // MODE_STATIC: static push-pull initialisation (also saturate t's in-edges)
+  int32_t bu_alpha;          // BFS: bottom-up when frontier slots x bu_alpha > unvisited slots (BU_ALPHA)
+  int32_t dense_div;         // BFS: top-down by stores + compaction when frontier slots x dense_div >= S (DENSE_DIV)
   int32_t async_sleep_ns;    // back-off of a warp waiting for a ring item
   int32_t async_tmax_any;    // 1: the time budget applies however much work is pending (repairs)
   int32_t *plist;            // region P of push-pull stage 2

@@ -1614,10 +1614,10 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
           ctl->bulc[2 * ((lvl + 1) & 1) + threadIdx.x] = 0;
         }
       }
-      const bool bu0 = f0 > 0 && (unsigned long long)f0 * BU_ALPHA > (unsigned long long)(mu[0] > 0 ? mu[0] : 0);
-      const bool bu1 = f1 > 0 && (unsigned long long)f1 * BU_ALPHA > (unsigned long long)(mu[1] > 0 ? mu[1] : 0);
-      const bool dn0 = !bu0 && f0 > 0 && (unsigned long long)f0 * DENSE_DIV >= (unsigned long long)d.S;
-      const bool dn1 = !bu1 && f1 > 0 && (unsigned long long)f1 * DENSE_DIV >= (unsigned long long)d.S;
+      const bool bu0 = f0 > 0 && (unsigned long long)f0 * d.bu_alpha > (unsigned long long)(mu[0] > 0 ? mu[0] : 0);
+      const bool bu1 = f1 > 0 && (unsigned long long)f1 * d.bu_alpha > (unsigned long long)(mu[1] > 0 ? mu[1] : 0);
+      const bool dn0 = !bu0 && f0 > 0 && (unsigned long long)f0 * d.dense_div >= (unsigned long long)d.S;
+      const bool dn1 = !bu1 && f1 > 0 && (unsigned long long)f1 * d.dense_div >= (unsigned long long)d.S;
       const BfsCtx ctx{lvl, collect, (bu0 ? 1u : 0u) | (bu1 ? 2u : 0u), (dn0 ? 1u : 0u) | (dn1 ? 2u : 0u),
                        BL{L.q((lvl + 1) & 1), qc + NB * ((lvl + 1) % 3), n, L.qc((lvl + 1) & 1)},
                        BL{L.wl0, wlc, n, L.cw0}, ctl->fs + 2 * ((lvl + 1) % 3)};
