@@ -1074,7 +1074,7 @@ __device__ __forceinline__ void discharge(const Dev &d, const G &g, Smem &sm, in
     }
   }
   if (d.async) {                        // every member's pushes land before u is released
-    __threadfence();
+    if (pushes > 0) __threadfence();
     g.sync();
   }
   if (g.rank() == 0) {
@@ -1135,11 +1135,19 @@ __device__ __forceinline__ void discharge_chunk(const Dev &d, Smem &sm, long lon
   const int32_t nch = (rend - rbeg + CH - 1) / CH;
   const unsigned long long t_start = d.trace ? gtimer() : 0;
   const int32_t hu = ldv(k.hgt + u);
+  if (lane == 0) DBG(d, 204, u, (int32_t)(ce >> 32), rend - rbeg, 0);
   uint32_t nmin = 0xffffffffu;           // lowest height among slots left residual
   unsigned long long pushes = 0, scanned = 0;
   bool dry = false;
   WarpG g{lane};
+  // excess already claimed by the other chunks (or drained): nothing to push here,
+  // and an admissible slot may remain -> no lift (dry); skips the slot loads
   if (hu < n) {
+    long long e0 = 0;
+    if (lane == 0) e0 = ldv(d.e + u) * k.sign;
+    dry = g.bcast(e0) <= 0;
+  }
+  if (hu < n && !dry) {
     for (int32_t b0 = beg; b0 < end; b0 += 128) {   // warp-uniform trip count (collectives inside)
       const int32_t i0 = b0 + lane;
       int32_t r[4], v[4], h[4], ri[4];
@@ -1190,7 +1198,7 @@ __device__ __forceinline__ void discharge_chunk(const Dev &d, Smem &sm, long lon
     }
   }
   nmin = (uint32_t)g.min(dry ? 0ull : (unsigned long long)nmin);
-  __threadfence();                       // every lane's pushes land before u can be taken again
+  if (g.any(pushes > 0)) __threadfence();   // every lane's pushes land before u can be taken again
   __syncwarp();
   if (lane == 0) {
     if (nmin < (uint32_t)DMIN_NONE) atomicMin(d.dmin + u, (int32_t)nmin);
@@ -1217,6 +1225,7 @@ __device__ __forceinline__ void discharge_chunk(const Dev &d, Smem &sm, long lon
       sstat_add(sm, ST_DIS_V, 1);
       sstat_add(sm, ST_RELABELS, lifts);
     }
+    DBG(d, 205, u, (int32_t)(ce >> 32), (int32_t)pushes, (int32_t)lifts);
     if (d.trace) {
       const unsigned long long dt = gtimer() - t_start;
       const unsigned long long key = (min(dt, 0xffffffffull) << 32) |
