@@ -119,8 +119,10 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def make_workload(rank: int, frac: float, nb: int, seed_base: int = 100):
-    g = W.rmat(20, 16, 1 + rank, 7)
+def make_workload(rank: int, frac: float, nb: int, seed_base: int = 100, scale: int = 20):
+    """RMAT-`scale` snapshot of this rank (graph seed 1 + rank) and its cumulative batches:
+    scale 20 = BASELINE config 2 (the default bench line), 22 = one config-5 snapshot."""
+    g = W.rmat(scale, 16, 1 + rank, 7)
     st = W.CapState(g)
     batches = []
     for j in range(nb):
@@ -150,7 +152,7 @@ def run_reference(args):
     import oracle as O
     O.build()
     nb = args.warmup + args.steps
-    g, batches = make_workload(0, args.frac, nb)
+    g, batches = make_workload(0, args.frac, nb, scale=20 if args.workload == "rmat20" else 22)
     st = W.CapState(g)
     times, k_tot = [], 0
     for j, b in enumerate(batches):
@@ -176,10 +178,13 @@ def run_reference(args):
 
 
 def config_dict(g, args, k):
-    return {"workload": "config2 RMAT-20 (2^20 V, ef 16, caps U[1,1000]) + cumulative 1% mixed batches",
+    wl = ("config2 RMAT-20 (2^20 V, ef 16, caps U[1,1000]) + cumulative 1% mixed batches" if args.workload == "rmat20"
+          else "config5 RMAT-22 snapshot per rank (2^22 V, ef 16, caps U[1,1000], graph seed 1 + rank) "
+               "+ cumulative 1% mixed batches")
+    return {"workload": wl,
             "n": int(g.n), "m": int(g.m), "batch_k": int(k), "batch_frac": args.frac, "algo": args.algo,
             "step": "dmf_apply_batch + dmf_min_cut_source_side" if not args.no_cut else "dmf_apply_batch",
-            "l2": "inputs larger than L2 (slot arrays 28 B/slot x 31.4M slots = 0.88 GB >> 126 MB L2)",
+            "l2": "inputs larger than L2 (slot arrays 28 B/slot x S slots: 0.88 GB (RMAT-20) / 3.6 GB (RMAT-22) >> 126 MB L2)",
             "parallelism": f"replicas x{args.gpus}"}
 
 
@@ -190,6 +195,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="dmf", choices=["dmf", "reference"])
     ap.add_argument("--algo", default="pp", choices=["pp", "pr"])
+    ap.add_argument("--workload", default="rmat20", choices=["rmat20", "rmat22"],
+                    help="rmat20 = BASELINE config 2 (default); rmat22 = config 5 (one RMAT-22 snapshot per rank)")
     ap.add_argument("--frac", type=float, default=0.01)
     ap.add_argument("--no-cut", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -215,7 +222,7 @@ def main():
 
     K, Wm = args.steps, args.warmup
     nb = Wm + 2 * K                       # warm-up, device-resident timed steps, e2e timed steps
-    g, batches = make_workload(rank, args.frac, nb)
+    g, batches = make_workload(rank, args.frac, nb, scale=20 if args.workload == "rmat20" else 22)
     f = P.DynMaxFlow.from_graph(g, algo=args.algo)
     stream = f.stream
 
@@ -319,7 +326,7 @@ def main():
         if world == 1 and not args.no_cpu_baseline:
             dt, Fo = cpu_oracle_sample(g, batches[0], args.oracle_algo)
             cpu = {"value": batches[0].k / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-                   "sample": f"one full {args.oracle_algo} recompute of RMAT-20 after batch 0 "
+                   "sample": f"one full {args.oracle_algo} recompute of {args.workload.upper()} after batch 0 "
                              f"(k={batches[0].k}), single thread, {dt:.2f} s"}
         ms_step = el_max / K
         static_alg1 = float(np.median(static_ms))
