@@ -350,6 +350,10 @@ def main():
             "cpu_baseline": cpu,
             "clocks": {k: clocks[k] for k in ("sm_mhz", "sm_max_mhz", "reasons")},
             "batch_apply_ms_median": apply_ms,
+            # device time of the e2e steps' own launches (later cumulative batches): separates the
+            # host-path overhead (copies, syncs) from the batches being different
+            "e2e_batch_device_ms_median": float(np.median([P.DynMaxFlow.stats_to_dict(raw[j])["device_ms"]
+                                                           for j in range(Wm + K, Wm + 2 * K)])),
             "static_solve_ms_median": static_med,
             "static_solve_ms_median_by_variant": {"alg1": static_alg1, "static_push_pull": static_pp},
             "speedup_vs_static": static_med / apply_ms,
