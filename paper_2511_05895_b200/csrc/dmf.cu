@@ -73,7 +73,8 @@ struct dmf_graph {
   int32_t async_warps = 8;   // DMF_ASYNC_WARPS
   int32_t bu_alpha = (int32_t)BU_ALPHA, dense_div = (int32_t)DENSE_DIV;   // DMF_BU_ALPHA, DMF_DENSE_DIV
   int32_t async_sleep_ns = 1024;   // DMF_ASYNC_SLEEP_NS
-  long long async_tmax_us = 300;   // DMF_ASYNC_TMAX_US
+  int32_t async_tmax_pend = 0x7fffffff;   // DMF_ASYNC_TMAX_PEND (repairs; static: 64)
+  long long async_tmax_us = 600;   // DMF_ASYNC_TMAX_US (measured: 300 cuts legitimate phases of later batches)
   long long budget_mul = 1;  // DMF_BUDGET_MUL: discharge work between global relabels, in whole-graph BFS units
   long long *e = nullptr;
   uint8_t *part = nullptr, *mask = nullptr, *rlf = nullptr;
@@ -237,6 +238,7 @@ static Dev make_dev(dmf_graph *g) {
   d.async_warps = g->async_warps;
   d.bu_alpha = g->bu_alpha; d.dense_div = g->dense_div;
   d.async_sleep_ns = g->async_sleep_ns;
+  d.async_tmax_pend = g->async_tmax_pend;
   d.async_tmax_ns = g->async_tmax_us * 1000LL;
   d.plist = g->plist; d.stamp = g->stamp;
   d.mask = g->mask; d.ctl = g->ctl;
@@ -482,7 +484,8 @@ int dmf_create(int32_t n, const int64_t *row_ptr, const int32_t *col, const int3
   if (const char *ba = getenv("DMF_BU_ALPHA")) g->bu_alpha = atoi(ba) > 0 ? atoi(ba) : g->bu_alpha;
   if (const char *dd = getenv("DMF_DENSE_DIV")) g->dense_div = atoi(dd) > 0 ? atoi(dd) : g->dense_div;
   if (const char *sl = getenv("DMF_ASYNC_SLEEP_NS")) g->async_sleep_ns = atoi(sl) > 0 ? atoi(sl) : 1024;
-  if (const char *tm = getenv("DMF_ASYNC_TMAX_US")) g->async_tmax_us = atoll(tm) > 0 ? atoll(tm) : 300;
+  if (const char *tp = getenv("DMF_ASYNC_TMAX_PEND")) g->async_tmax_pend = atoi(tp) > 0 ? atoi(tp) : 0x7fffffff;
+  if (const char *tm = getenv("DMF_ASYNC_TMAX_US")) g->async_tmax_us = atoll(tm) > 0 ? atoll(tm) : 600;
   if (const char *bm = getenv("DMF_BUDGET_MUL")) g->budget_mul = atoll(bm) > 0 ? atoll(bm) : 1;
   if (const char *wd = getenv("DMF_WATCHDOG_S")) {
     g->watchdog_s = atof(wd);

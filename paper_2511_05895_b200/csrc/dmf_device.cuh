@@ -115,6 +115,7 @@ struct Dev {
   int32_t bu_alpha;          // BFS: bottom-up when frontier slots x bu_alpha > unvisited slots (BU_ALPHA)
   int32_t dense_div;         // BFS: top-down by stores + compaction when frontier slots x dense_div >= S (DENSE_DIV)
   int32_t async_sleep_ns;    // back-off of a warp waiting for a ring item
+  int32_t async_tmax_pend;   // repairs: the time budget stops a phase only while <= this many items are pending
   int32_t async_tmax_any;    // 1: the time budget applies however much work is pending (repairs)
   int32_t *plist;            // region P of push-pull stage 2
   int32_t *stamp;            // per-slot batch stamp (duplicate detection)

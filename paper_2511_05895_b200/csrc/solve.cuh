@@ -1434,7 +1434,8 @@ __device__ __forceinline__ void async_phase(const Dev &d, Smem &sm, const BL &in
       // relabel fixes every height at once
       // (a repair after a batch: always; the static solve from zero flow: only while
       // little is pending -- a long phase with plenty of parallel work is useful there)
-      if (!stop && (d.async_tmax_any || (uint32_t)old <= 64u) && gtimer() - sm.astart > (unsigned long long)d.async_tmax_ns)
+      if (!stop && (uint32_t)old <= (uint32_t)(d.async_tmax_any ? d.async_tmax_pend : 64) &&
+          gtimer() - sm.astart > (unsigned long long)d.async_tmax_ns)
         stop = true;
       if (!stop && sm.work > 32768ull) {                                  // budget: flushed in 32K-slot units
         const unsigned long long w = atomicExch(&sm.work, 0ull);
