@@ -59,6 +59,30 @@ def algorithmic_bytes(st: dict, n: int) -> int:
                + st["batch_entries"] * B_BATCH_ENTRY + st["reset_vertices"] * B_RESET_VERTEX + n * 9)
 
 
+def phase_roofline(per: list, peak: float) -> dict:
+    """Per-step achieved algorithmic GB/s of the three method steps the north star names,
+    from the in-kernel phase clock (one persistent kernel: ncu cannot split its phases):
+    global relabel (BFS levels + RESET), discharge (+ RIE), batch update (prologue).
+    Medians over the timed steps; frac against the same measured HBM peak."""
+    def row(bytes_fn, us_keys):
+        vals = []
+        for p_ in per:
+            us = sum(p_[k] for k in us_keys)
+            if us > 0:
+                vals.append(bytes_fn(p_) / (us * 1e-6) / 1e9)
+        a = float(np.median(vals)) if vals else 0.0
+        return {"achieved_gbs": a, "frac": a / peak if peak else None,
+                "us_median": float(np.median([sum(p_[k] for k in us_keys) for p_ in per]))}
+    return {
+        "global_relabel": row(lambda p_: p_["bfs_vertices"] * B_BFS_VERTEX + p_["bfs_slots"] * B_BFS_SLOT
+                              + p_["reset_vertices"] * B_RESET_VERTEX, ("t_bfs_us", "t_reset_us")),
+        "discharge": row(lambda p_: p_["discharge_vertices"] * B_DIS_VERTEX + p_["discharge_slots"] * B_DIS_SLOT
+                         + p_["pushes"] * B_PUSH + p_["rie_slots"] * B_RIE_SLOT, ("t_discharge_us", "t_rie_us")),
+        "batch_update": row(lambda p_: p_["batch_entries"] * B_BATCH_ENTRY, ("t_prologue_us",)),
+        "note": "phase clock = block 0's barrier-to-barrier laps; bytes = SURVEY 8(d) unit costs x the phase's counters",
+    }
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -343,6 +367,7 @@ def main():
                     "h2d_bytes_per_step": int(3 * 4 * batches[0].k),
                     "d2h_bytes_per_step": int(8 + (0 if args.no_cut else g.n))},
             "gpu_launches": int(launches),
+            "phase_roofline": phase_roofline(per, peak),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": f"k_solve (mode {args.algo.upper()} batch launch)",
