@@ -45,7 +45,12 @@ typedef enum {
     DMF_ENOMEM = -5,     /* device allocation failed */
     DMF_ECUDA = -6,      /* CUDA runtime error (message in dmf_last_error) */
     DMF_EOVERFLOW = -7,  /* merged capacity of a pair exceeds DMF_CAP_MAX, or too many slots (>= 2^31) */
-    DMF_ENOCONV = -8     /* iteration cap reached (never expected; Thm P:318-330 bounds the work) */
+    DMF_ENOCONV = -8,    /* iteration cap reached (never expected; Thm P:318-330 bounds the work).
+                            The handle then holds a valid but NOT converged pseudoflow: flow / cut
+                            queries and DMF_DYN_PP return DMF_ESTATE until a dmf_static_solve or a
+                            DMF_DYN_PR repair (which converges from any valid pseudoflow) succeeds. */
+    DMF_ECHECK = -9      /* check_level > 0 and a device invariant check failed (a bug; the handle
+                            is marked not converged as for DMF_ENOCONV) */
 } dmf_status;
 
 typedef enum {
@@ -57,17 +62,52 @@ typedef enum {
  * residual fits int32. */
 #define DMF_CAP_MAX 1073741823
 
+/* Discharge schedules (dmf_options.schedule).  Every schedule computes the same F,
+ * S_min and S_max; they differ only in how active vertices are found and ordered. */
+typedef enum {
+    DMF_SCHED_AUTO = 0,      /* repairs: ASYNC; static solve: ROUNDS with the topology auto-switch */
+    DMF_SCHED_ASYNC = 1,     /* data-driven worklist seeding a device-wide ring queue: a vertex
+                                made active by a push is processed at once (the property P:647 credits
+                                to the topology-driven schedule) */
+    DMF_SCHED_ROUNDS = 2,    /* data-driven worklist, barrier-separated rounds */
+    DMF_SCHED_TOPOLOGY = 3   /* topology-driven rounds: every round sweeps all vertices of the
+                                domain and discharges the active ones in place; no worklist */
+} dmf_schedule;
+
 typedef struct {
     int32_t kernel_cycles;  /* KERNELCYCLES of Alg.2/Alg.6; 0 => max(1, floor(m/n)) (R17) */
     int32_t algo;           /* default algorithm for dmf_apply_batch when its algo argument is < 0 */
     int32_t max_iters;      /* cap on outer loop iterations per call; 0 => 4*n + 64 */
     int32_t grid_blocks;    /* 0 => occupancy-derived cooperative grid (multiple of the SM count) */
-    void *stream;           /* cudaStream_t for all work; NULL => a stream owned by the handle */
+    void *stream;           /* cudaStream_t for all work; NULL => a stream owned by the handle.
+                               cudaStreamLegacy ((void*)1) selects the legacy default stream. */
     /* Optional device allocator (e.g. the torch caching allocator); NULL => cudaMalloc.
      * alloc returns a device pointer of >= bytes (256-byte aligned) or NULL. */
     void *(*alloc)(size_t bytes, void *ctx);
     void (*free)(void *ptr, size_t bytes, void *ctx);
     void *alloc_ctx;
+    /* ---- engine knobs, per handle.  0 selects the default.  None of them changes a
+     * result (F, S_min, S_max are unique); they change the work schedule only.  The
+     * environment variable in brackets, when set, overrides the field (experiments). */
+    int32_t schedule;       /* dmf_schedule [DMF_SCHED] */
+    int32_t async_warps;    /* consumer warps per CTA in the ASYNC phase, 1..16; 0 => 8 [DMF_ASYNC_WARPS] */
+    int32_t budget_mul;     /* discharge work allowed between two global relabels, in units of one
+                               whole-graph BFS (S + 6n slot visits); 0 => 1; < 0 divides the unit
+                               by -budget_mul (tests force budget stops with it) [DMF_BUDGET_MUL] */
+    int32_t tail_items;     /* progress stop of an ASYNC phase: once at most 64 items are pending, this
+                               many further item completions hand the rest to a global relabel;
+                               0 => 2048, < 0 => never [DMF_TAIL_ITEMS] */
+    int32_t local_gap;      /* R14 form 2, the local gap exit inside a discharge phase (per-level
+                               counts): 0 => on, < 0 => off [DMF_LOCAL_GAP] */
+    int32_t warm;           /* DYN_PP after DYN_PP starts from the previous call's labels: 0 => on,
+                               < 0 => off (every repair starts with a fresh global relabel) [DMF_WARM] */
+    int32_t topo_div;       /* ROUNDS/AUTO: a round runs topology-driven when more than n / topo_div
+                               vertices are active; 0 => 16, < 0 => never [DMF_TOPO_DIV] */
+    int32_t check_level;    /* 0 => off; 1 => after every solve / repair the device checks the cheap
+                               invariants (0 <= res <= cap + cap_rev, res[i] + res[rev[i]] = cap[i] +
+                               cap[rev[i]], mirror consistency, sum of e = 0) and the call fails with
+                               DMF_ECHECK if one is violated [DMF_CHECK_LEVEL] */
+    int32_t reserved[8];    /* must be zero */
 } dmf_options;
 
 typedef struct {
@@ -99,6 +139,11 @@ typedef struct {
      * prologue = batch validate/apply/clamp + source / S->T saturation,
      * epilogue = P extraction, partitions, flow reduction, cut masks */
     float   t_prologue_us, t_reset_us, t_bfs_us, t_discharge_us, t_rie_us, t_epilogue_us;
+    int64_t gap_levels;        /* R14 form 2: height levels found emptied by a lift (local gap) */
+    int64_t gap_skips;         /* discharges stopped because the vertex sat above an emptied level */
+    int64_t topology_rounds;   /* discharge rounds run topology-driven */
+    int64_t tail_stops;        /* ASYNC phases ended by the progress stop (tail_items) */
+    int64_t stage2_skipped;    /* DYN_PP: stage 2 / the P-reach skipped (P holds no deficit / no excess) */
 } dmf_stats;
 
 /* Fill *opt with defaults (all zero / NULL; algo = DMF_DYN_PP). */
@@ -193,6 +238,25 @@ int dmf_sizes(const dmf_graph *g, int32_t *n, int64_t *S, int64_t *m);
  * rev[i] = slot of the reverse pair), excess int64[n].  For checkers. */
 int dmf_export_state(const dmf_graph *g, int64_t *row_ptr, int32_t *dst, int32_t *rev,
                      int32_t *cap, int32_t *res, int64_t *excess);
+
+/* Checkpoint restore (SURVEY §5 "Checkpoint / resume": the converged residual graph IS
+ * the state carried between batches).  cap, res: int32[S] and excess: int64[n]
+ * (host or device) in the slot order of dmf_export_state of a handle built from the
+ * SAME input graph (same n, row_ptr, col; capacities may differ).  The imported state
+ * is validated on the device with the invariant check of check_level 1 plus
+ * e(v) = sum over the slots j of v of (res[j] - cap[j]) (net inflow);
+ * DMF_EINVAL if it fails, with the handle's previous state restored.  On success the
+ * handle holds a valid pseudoflow that is NOT yet known to be converged: flow and cut
+ * queries return DMF_ESTATE until dmf_static_solve or a DMF_DYN_PR batch (k = 0 is
+ * allowed) has repaired it -- a Dynamic Push-Relabel repair converges from any valid
+ * pseudoflow (the sink set {t} u deficient vertices, reading R2). */
+int dmf_import_state(dmf_graph *g, const int32_t *cap, const int32_t *res, const int64_t *excess);
+
+/* Run the device invariant check of check_level 1 on the current state now:
+ * 0 <= res <= cap + cap_rev, res[i] + res[rev[i]] = cap[i] + cap[rev[i]], rres[i] =
+ * res[rev[i]], e(v) = sum_{slots j of v} (res[j] - cap[j]), sum of e = 0.  DMF_OK or
+ * DMF_ECHECK (message names the first violated invariant and a witness). */
+int dmf_check_state(dmf_graph *g);
 
 /* Stage (ii): turn the converged pseudoflow
  * into a true maximum flow in place.  Stuck excess is returned to s (every vertex with

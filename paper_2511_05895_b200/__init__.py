@@ -23,7 +23,8 @@ __all__ = ["DynMaxFlow", "DMFError", "load_library", "DYN_PR", "DYN_PP", "CAP_MA
 DYN_PR, DYN_PP = 0, 1
 CAP_MAX = 1073741823
 STATUS = {0: "DMF_OK", -1: "DMF_EINVAL", -2: "DMF_ENOSLOT", -3: "DMF_EDUP", -4: "DMF_ESTATE",
-          -5: "DMF_ENOMEM", -6: "DMF_ECUDA", -7: "DMF_EOVERFLOW", -8: "DMF_ENOCONV"}
+          -5: "DMF_ENOMEM", -6: "DMF_ECUDA", -7: "DMF_EOVERFLOW", -8: "DMF_ENOCONV", -9: "DMF_ECHECK"}
+SCHED = {"auto": 0, "async": 1, "rounds": 2, "topology": 3}
 _ALGO = {"pr": DYN_PR, "pp": DYN_PP, DYN_PR: DYN_PR, DYN_PP: DYN_PP}
 
 _ALLOC_T = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
@@ -31,9 +32,16 @@ _FREE_T = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void
 
 
 class Options(ctypes.Structure):
+    """dmf_options (include/dmf.h): field order and types mirror the C struct."""
     _fields_ = [("kernel_cycles", ctypes.c_int32), ("algo", ctypes.c_int32), ("max_iters", ctypes.c_int32),
                 ("grid_blocks", ctypes.c_int32), ("stream", ctypes.c_void_p), ("alloc", _ALLOC_T),
-                ("free", _FREE_T), ("alloc_ctx", ctypes.c_void_p)]
+                ("free", _FREE_T), ("alloc_ctx", ctypes.c_void_p),
+                ("schedule", ctypes.c_int32), ("async_warps", ctypes.c_int32), ("budget_mul", ctypes.c_int32),
+                ("tail_items", ctypes.c_int32), ("local_gap", ctypes.c_int32), ("warm", ctypes.c_int32),
+                ("topo_div", ctypes.c_int32), ("check_level", ctypes.c_int32), ("reserved", ctypes.c_int32 * 8)]
+
+
+KNOBS = ("schedule", "async_warps", "budget_mul", "tail_items", "local_gap", "warm", "topo_div", "check_level")
 
 
 class Stats(ctypes.Structure):
@@ -49,7 +57,8 @@ class Stats(ctypes.Structure):
                 ("kernel_launches", ctypes.c_int64),
                 ("device_ms", ctypes.c_float), ("t_prologue_us", ctypes.c_float), ("t_reset_us", ctypes.c_float),
                 ("t_bfs_us", ctypes.c_float), ("t_discharge_us", ctypes.c_float), ("t_rie_us", ctypes.c_float),
-                ("t_epilogue_us", ctypes.c_float)]
+                ("t_epilogue_us", ctypes.c_float), ("gap_levels", ctypes.c_int64), ("gap_skips", ctypes.c_int64),
+                ("topology_rounds", ctypes.c_int64), ("tail_stops", ctypes.c_int64), ("stage2_skipped", ctypes.c_int64)]
 
 
 class DMFError(RuntimeError):
@@ -84,6 +93,8 @@ def load_library():
         L.dmf_export_state.argtypes = [P, P, P, P, P, P, P]
         L.dmf_export_labels.argtypes = [P, P, P, P, P]
         L.dmf_to_flow.argtypes = [P]
+        L.dmf_import_state.argtypes = [P, P, P, P]
+        L.dmf_check_state.argtypes = [P]
         L.dmf_static_solve_pp.argtypes = [P]
         L.dmf_edge_flow.argtypes = [P, P]
         L.dmf_set_trace.argtypes = [P, I32]
@@ -94,6 +105,7 @@ def load_library():
         L.dmf_last_error.restype = ctypes.c_char_p
         for f in ("dmf_create", "dmf_static_solve", "dmf_static_solve_pp", "dmf_apply_batch", "dmf_flow_value", "dmf_min_cut_source_side",
                   "dmf_max_cut_source_side", "dmf_get_stats", "dmf_sizes", "dmf_export_state", "dmf_export_labels", "dmf_to_flow", "dmf_edge_flow", "dmf_set_trace",
+                  "dmf_import_state", "dmf_check_state",
                   "dmf_get_trace", "dmf_get_trace_cta"):
             getattr(L, f).restype = ctypes.c_int
         _lib = L
@@ -109,11 +121,18 @@ def _ptr(a):
     return ctypes.c_void_p(a.data_ptr())
 
 
-def _i32(a):
+def _i32(a, name="array"):
+    """int32, contiguous, 1-D: numpy arrays are converted, torch tensors must already be."""
     if isinstance(a, np.ndarray):
-        return np.ascontiguousarray(a, np.int32)
-    import torch
-    assert a.dtype == torch.int32 and a.is_contiguous()
+        a = np.ascontiguousarray(a, np.int32)
+    else:
+        import torch
+        if not isinstance(a, torch.Tensor):
+            a = np.ascontiguousarray(np.asarray(a), np.int32)
+        elif a.dtype != torch.int32 or not a.is_contiguous():
+            raise TypeError(f"{name}: torch tensors must be contiguous int32 (got {a.dtype}, contiguous={a.is_contiguous()})")
+    if a.ndim != 1:
+        raise ValueError(f"{name}: expected a 1-D array, got shape {tuple(a.shape)}")
     return a
 
 
@@ -127,7 +146,7 @@ class DynMaxFlow:
     """
 
     def __init__(self, n, row_ptr, col, cap, s, t, kernel_cycles=0, algo="pp", max_iters=0, grid_blocks=0,
-                 torch_alloc=True, stream=None):
+                 torch_alloc=True, stream=None, **knobs):
         L = load_library()
         import torch
         if not torch.cuda.is_available():
@@ -140,10 +159,17 @@ class DynMaxFlow:
         opt.algo = _ALGO[algo]
         opt.max_iters = max_iters
         opt.grid_blocks = grid_blocks
+        for k, val in knobs.items():          # per-handle engine knobs (dmf_options; include/dmf.h)
+            if k not in KNOBS:
+                raise TypeError(f"unknown option {k!r} (expected one of {KNOBS})")
+            setattr(opt, k, SCHED[val] if k == "schedule" and isinstance(val, str) else int(val))
         if stream is None:
             stream = torch.cuda.current_stream()
         self.stream = stream
-        opt.stream = ctypes.c_void_p(stream.cuda_stream)
+        # torch's default stream has handle 0, which the library would read as "create
+        # my own stream": pass cudaStreamLegacy instead so that library work stays
+        # ordered with torch work on the default stream
+        opt.stream = ctypes.c_void_p(stream.cuda_stream if stream.cuda_stream else 1)
         self._cbs = None
         if torch_alloc:
             dev = torch.cuda.current_device()
@@ -164,8 +190,10 @@ class DynMaxFlow:
             self._cbs = (_ALLOC_T(_alloc), _FREE_T(_free))
             opt.alloc, opt.free = self._cbs
         rp = np.ascontiguousarray(row_ptr, np.int64) if isinstance(row_ptr, np.ndarray) else row_ptr
-        col = _i32(col)
-        cap = _i32(cap)
+        col = _i32(col, "col")
+        cap = _i32(cap, "cap")
+        if col.shape[0] != cap.shape[0]:
+            raise ValueError(f"col and cap differ in length ({col.shape[0]} vs {cap.shape[0]})")
         h = ctypes.c_void_p()
         rc = L.dmf_create(int(n), _ptr(rp), _ptr(col), _ptr(cap), int(s), int(t), ctypes.byref(opt), ctypes.byref(h))
         self._check(rc)
@@ -199,8 +227,10 @@ class DynMaxFlow:
         return self.flow_value()
 
     def apply_batch(self, u, v, new_cap, algo=None) -> int:
-        u, v, c = _i32(u), _i32(v), _i32(new_cap)
+        u, v, c = _i32(u, "u"), _i32(v, "v"), _i32(new_cap, "new_cap")
         k = int(u.shape[0])
+        if v.shape[0] != k or c.shape[0] != k:
+            raise ValueError(f"u, v, new_cap must have equal lengths (got {k}, {v.shape[0]}, {c.shape[0]})")
         a = -1 if algo is None else _ALGO[algo]
         self._check(self._L.dmf_apply_batch(self._h, k, _ptr(u), _ptr(v), _ptr(c), a))
         return self.flow_value()
@@ -273,6 +303,19 @@ class DynMaxFlow:
         e = np.zeros(self.n, np.int64)
         self._check(self._L.dmf_export_state(self._h, _ptr(row_ptr), _ptr(dst), _ptr(rev), _ptr(cap), _ptr(res), _ptr(e)))
         return dict(row_ptr=row_ptr, dst=dst, rev=rev, cap=cap, res=res, e=e)
+
+    def import_state(self, cap, res, excess):
+        """dmf_import_state: restore (cap, res, excess) exported from a handle of the same
+        input graph; the state is then valid but not converged (repair with a DYN_PR batch)."""
+        cap, res = _i32(cap, "cap"), _i32(res, "res")
+        e = np.ascontiguousarray(excess, np.int64) if isinstance(excess, np.ndarray) else excess
+        if cap.shape[0] != self.S or res.shape[0] != self.S or e.shape[0] != self.n:
+            raise ValueError("import_state: cap/res need S entries and excess n entries")
+        self._check(self._L.dmf_import_state(self._h, _ptr(cap), _ptr(res), _ptr(e)))
+
+    def check_state(self):
+        """dmf_check_state: device invariant check of the current state (raises DMFError)."""
+        self._check(self._L.dmf_check_state(self._h))
 
     def to_flow(self) -> int:
         """Stage (ii): convert the state into a true maximum flow (dmf_to_flow); returns F."""

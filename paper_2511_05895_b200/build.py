@@ -4,7 +4,10 @@ import subprocess
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
-LIB = os.path.join(PKG, "libdmf.so")
+# DMF_LIB / DMF_EXTRA_NVCC select a diagnostic variant (e.g. -DDMF_DEBUG_BUSY into
+# libdmf_debug.so); the product build is libdmf.so with the flags below.
+LIB = os.environ.get("DMF_LIB") or os.path.join(PKG, "libdmf.so")
+EXTRA = os.environ.get("DMF_EXTRA_NVCC", "").split()
 SRC_DIR = os.path.join(PKG, "csrc")
 SOURCES = [os.path.join(SRC_DIR, f) for f in ("dmf.cu",)]
 DEPS = SOURCES + [os.path.join(SRC_DIR, f) for f in ("dmf_device.cuh", "solve.cuh")] + [os.path.join(ROOT, "include", "dmf.h")]
@@ -22,7 +25,7 @@ def stale() -> bool:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if force or stale():
-        cmd = [NVCC, *FLAGS, "-I", os.path.join(ROOT, "include"), "-o", LIB, *SOURCES]
+        cmd = [NVCC, *FLAGS, *EXTRA, "-I", os.path.join(ROOT, "include"), "-o", LIB, *SOURCES]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError("nvcc failed:\n" + r.stderr[-4000:])

@@ -68,14 +68,19 @@ struct dmf_graph {
   int32_t *dcnt = nullptr, *dmin = nullptr;
   long long *aq = nullptr;
   int32_t aq_mask = 0;
-  bool async = true;         // repairs (DYN_PR / DYN_PP): asynchronous discharge; DMF_ASYNC=0: rounds
-  bool async_static = false; // static solve from zero flow: rounds (massively parallel work); DMF_ASYNC_STATIC=1: async
-  int32_t async_warps = 8;   // DMF_ASYNC_WARPS
-  int32_t bu_alpha = (int32_t)BU_ALPHA, dense_div = (int32_t)DENSE_DIV;   // DMF_BU_ALPHA, DMF_DENSE_DIV
-  int32_t async_sleep_ns = 1024;   // DMF_ASYNC_SLEEP_NS
-  int32_t async_tmax_pend = 0x7fffffff;   // DMF_ASYNC_TMAX_PEND (repairs; static: 64)
-  long long async_tmax_us = 600;   // DMF_ASYNC_TMAX_US (measured: 300 cuts legitimate phases of later batches)
-  long long budget_mul = 1;  // DMF_BUDGET_MUL: discharge work between global relabels, in whole-graph BFS units
+  // engine knobs, resolved from dmf_options (+ DMF_* environment overrides) in dmf_create
+  bool async = true;         // repairs (DYN_PR / DYN_PP): asynchronous discharge (else rounds)
+  bool async_static = false; // static solve from zero flow: rounds (massively parallel work)
+  int32_t async_warps = 8;
+  int32_t bu_alpha = (int32_t)BU_ALPHA, dense_div = (int32_t)DENSE_DIV;
+  int32_t async_sleep_ns = 1024;
+  int32_t tail_items = 2048;
+  int32_t local_gap = 1;
+  int32_t topo_div = 16;
+  int32_t check_level = 0;
+  long long budget_mul = 1;
+  int32_t *cnt = nullptr, *cnt_next = nullptr;   // local-gap level counts (this call / next warm call)
+  int32_t *chk = nullptr;                          // invariant check scratch (64 bytes)
   long long *e = nullptr;
   uint8_t *part = nullptr, *mask = nullptr, *rlf = nullptr;
   int32_t *bbuf = nullptr;   // batch staging: u, v, c, slot  (4 * bcap)
@@ -93,7 +98,7 @@ struct dmf_graph {
   bool solved = false;
   bool smin_valid = false;   // g->mask holds S_min of the current state
   bool warm = false;         // hp/hm/part hold the final labels of the last DYN_PP repair
-  bool no_warm = false;      // DMF_NO_WARM=1: always run stage 1's initial global relabel
+  bool no_warm = false;      // options.warm < 0: always run stage 1's initial global relabel
   int64_t launches = 0;      // kernels launched by solve / apply / cut calls since create
   int64_t flow = 0;
   dmf_stats stats{};
@@ -210,6 +215,44 @@ __global__ void k_sum_i32(int64_t N, const int32_t *a, unsigned long long *out) 
   if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
 }
 
+// Invariant check (check_level 1, dmf_check_state, dmf_import_state): writes the first
+// violated check code and a witness index to out[0..1].
+//   1: 0 <= res[i] <= cap[i] + cap[rev[i]]        (capacity)
+//   2: res[i] + res[rev[i]] == cap[i] + cap[rev[i]] (pair sum)
+//   3: rres[i] == res[rev[i]]                    (mirror; skipped when rres is NULL)
+//   4: e(v) == sum over the slots j of v of (res[j] - cap[j])   (net inflow)
+// and accumulates sum(e) into *esum (check 5 on the host: sum of e == 0).
+__device__ void chk_report(int32_t *out, int32_t code, long long at) {
+  if (atomicCAS(out, 0, code) == 0) out[1] = (int32_t)at;
+}
+__global__ void k_check(int32_t n, int64_t S, const int32_t *row, const int32_t *rev, const int32_t *cap,
+                        const int32_t *res, const int32_t *rres, const long long *e, int32_t *out,
+                        unsigned long long *esum) {
+  const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = gt; i < S; i += nt) {
+    const int32_t ri = rev[i];
+    const long long c = (long long)cap[i] + cap[ri], r = res[i];
+    if (r < 0 || r > c) chk_report(out, 1, i);
+    if (r + res[ri] != c) chk_report(out, 2, i);
+    if (rres && rres[i] != res[ri]) chk_report(out, 3, i);
+  }
+  const int lane = threadIdx.x & 31;
+  for (int64_t v = gt >> 5; v < n; v += nt >> 5) {      // warp per vertex
+    long long sum = 0;
+    for (int32_t j = row[v] + lane; j < row[v + 1]; j += 32) sum += (long long)res[j] - cap[j];
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0) {
+      if (sum != e[v]) chk_report(out, 4, v);
+      atomicAdd(esum, (unsigned long long)e[v]);
+    }
+  }
+}
+
+__global__ void k_mirror(int64_t S, const int32_t *rev, const int32_t *res, int32_t *rres) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < S; i += (int64_t)gridDim.x * blockDim.x)
+    rres[i] = res[rev[i]];
+}
+
 int bits_for(unsigned long long x) {
   int b = 1;
   while (b < 64 && (x >> b)) b++;
@@ -226,7 +269,8 @@ static Dev make_dev(dmf_graph *g) {
   d.max_iters = g->opt.max_iters > 0 ? g->opt.max_iters : (int32_t)(4LL * g->n + 64 > 0x3fffffff ? 0x3fffffff : 4LL * g->n + 64);
   d.batch_id = g->batch_id;
   d.warm = g->warm ? 1 : 0;
-  d.work_budget = (g->S + 6LL * g->n) * g->budget_mul;   // ~ the cost of one whole-graph global relabel
+  // ~ the cost of one whole-graph global relabel, times budget_mul (or divided by -budget_mul)
+  d.work_budget = g->budget_mul > 0 ? (g->S + 6LL * g->n) * g->budget_mul : (g->S + 6LL * g->n) / -g->budget_mul;
   d.S = g->S; d.k = 0;
   d.row = g->row; d.dst = g->dst; d.rev = g->rev; d.cap = g->cap; d.res = g->res; d.rres = g->rres;
   d.e = g->e; d.hp = g->hp; d.hm = g->hm; d.part = g->part;
@@ -238,8 +282,9 @@ static Dev make_dev(dmf_graph *g) {
   d.async_warps = g->async_warps;
   d.bu_alpha = g->bu_alpha; d.dense_div = g->dense_div;
   d.async_sleep_ns = g->async_sleep_ns;
-  d.async_tmax_pend = g->async_tmax_pend;
-  d.async_tmax_ns = g->async_tmax_us * 1000LL;
+  d.cnt = g->cnt; d.cnt_next = g->cnt_next;
+  d.local_gap = g->local_gap; d.topo_div = g->topo_div; d.tail_items = g->tail_items;
+  d.check_level = g->check_level;
   d.plist = g->plist; d.stamp = g->stamp;
   d.mask = g->mask; d.ctl = g->ctl;
   d.dbg = g->ddbg;
@@ -249,6 +294,35 @@ static Dev make_dev(dmf_graph *g) {
   return d;
 }
 
+static const char *check_name(int32_t code) {
+  switch (code) {
+    case 1: return "capacity: res outside [0, cap + cap_rev] at slot";
+    case 2: return "pair sum: res + res_rev != cap + cap_rev at slot";
+    case 3: return "mirror: rres != res[rev] at slot";
+    case 4: return "excess: e(v) != net inflow at vertex";
+    case 5: return "excess: sum of e != 0";
+    default: return "invariant";
+  }
+}
+
+// Device invariant check of (cap, res, rres, e); DMF_OK or DMF_ECHECK.
+static int check_arrays(dmf_graph *g, const int32_t *cap, const int32_t *res, const int32_t *rres, const long long *e) {
+  CK(cudaMemsetAsync(g->chk, 0, 64, g->stream));
+  const int blocks = g->grid_blocks > 0 ? g->grid_blocks : 296;
+  k_check<<<blocks, 512, 0, g->stream>>>(g->n, g->S, g->row, g->rev, cap, res, rres, e, g->chk,
+                                          reinterpret_cast<unsigned long long *>(g->chk + 8));
+  CK(cudaGetLastError());
+  int32_t h[16];
+  CK(cudaMemcpyAsync(h, g->chk, 64, cudaMemcpyDeviceToHost, g->stream));
+  CK(cudaStreamSynchronize(g->stream));
+  long long esum = 0;
+  memcpy(&esum, h + 8, 8);
+  if (h[0]) return fail(DMF_ECHECK, "%s %d", check_name(h[0]), h[1]);
+  if (esum != 0) return fail(DMF_ECHECK, "%s (%lld)", check_name(5), esum);
+  return DMF_OK;
+}
+static int check_state(dmf_graph *g) { return check_arrays(g, g->cap, g->res, g->rres, g->e); }
+
 static int run_solve(dmf_graph *g, int32_t mode, const Dev &dv) {
   Dev d = dv;
   const bool smin_before = g->smin_valid;
@@ -257,7 +331,6 @@ static int run_solve(dmf_graph *g, int32_t mode, const Dev &dv) {
   g->warm = false;                                  // every launch rewrites hp or hm
   CK(cudaMemsetAsync(g->ctl, 0, sizeof(Ctl), g->stream));
   CK(cudaEventRecord(g->ev0, g->stream));
-  d.async_tmax_any = mode == MODE_STATIC ? 0 : 1;
   d.async = (mode == MODE_STATIC ? g->async_static : g->async) ? 1 : 0;
   int32_t md = mode;
   void *args[] = {&d, &md};
@@ -309,6 +382,11 @@ static int run_solve(dmf_graph *g, int32_t mode, const Dev &dv) {
   st.t_discharge_us = c.stat[ST_T_DIS] * 1e-3f;
   st.t_rie_us = c.stat[ST_T_RIE] * 1e-3f;
   st.t_epilogue_us = c.stat[ST_T_EPI] * 1e-3f;
+  st.gap_levels = (int64_t)c.stat[ST_GAP_LEVELS];
+  st.gap_skips = (int64_t)c.stat[ST_GAP_SKIPS];
+  st.topology_rounds = (int64_t)c.stat[ST_TOPO_ROUNDS];
+  st.tail_stops = (int64_t)c.stat[ST_TAIL_STOPS];
+  st.stage2_skipped = (int64_t)c.stat[ST_S2_SKIP];
   st.batch_entries = dv.k;
   st.device_ms = ms;
   if (c.pad != 0) fprintf(stderr, "[dmf debug] vertex %d discharged concurrently\n", c.pad - 1);
@@ -318,11 +396,24 @@ static int run_solve(dmf_graph *g, int32_t mode, const Dev &dv) {
                      : c.status == DMF_EINVAL ? "vertex id out of range"
                      : c.status == DMF_EOVERFLOW ? "capacity outside [0, DMF_CAP_MAX]"
                      : c.status == DMF_ENOCONV ? "iteration cap reached" : "error";
-    if (c.status != DMF_ENOCONV) g->warm = warm_before;   // rejected before any mutation
+    if (c.status != DMF_ENOCONV) {                  // rejected before any mutation: state unchanged
+      g->warm = warm_before;
+      g->smin_valid = smin_before;
+    } else {                                        // a partial repair: no converged state any more
+      g->solved = false;
+      g->smin_valid = false;
+      // the loop stopped after a global relabel had queued its worklist: drop the
+      // queued flags so that the next call starts clean
+      CK(cudaMemsetAsync(g->inq, 0, (size_t)g->n * 4, g->stream));
+      CK(cudaMemsetAsync(g->rlf, 0, (size_t)g->n, g->stream));
+      CK(cudaStreamSynchronize(g->stream));
+    }
     return fail(c.status, "%s (batch entry %d)", what, c.err_entry);
   }
-  if (mode == MODE_FLOW && c.flow != g->flow)
+  if (mode == MODE_FLOW && c.flow != g->flow) {
+    g->solved = false;
     return fail(DMF_ENOCONV, "stage (ii) changed F (%lld -> %lld)", (long long)g->flow, (long long)c.flow);
+  }
   if (mode == MODE_STATIC || mode == MODE_PR || mode == MODE_PP) {
     g->flow = c.flow;
     g->solved = true;
@@ -331,6 +422,11 @@ static int run_solve(dmf_graph *g, int32_t mode, const Dev &dv) {
   // inside S_max and inside T, and S_min of a maximum flow is unique)
   g->smin_valid = mode == MODE_PP || mode == MODE_MINCUT || (mode == MODE_FLOW && smin_before);
   g->warm = mode == MODE_PP && !g->no_warm;
+  if (g->warm && g->local_gap) std::swap(g->cnt, g->cnt_next);   // the final labels' histogram
+  if (g->check_level > 0 && mode != MODE_MINCUT && mode != MODE_MAXCUT) {
+    const int rc = check_state(g);
+    if (rc != DMF_OK) { g->solved = false; g->smin_valid = false; g->warm = false; return rc; }
+  }
   return DMF_OK;
 }
 
@@ -477,16 +573,44 @@ int dmf_create(int32_t n, const int64_t *row_ptr, const int32_t *col, const int3
     return bail(DMF_ENOMEM);
   }
   CKB(cudaMallocHost((void **)&g->hctl, sizeof(Ctl)));
-  if (const char *nw = getenv("DMF_NO_WARM")) g->no_warm = atoi(nw) != 0;
-  if (const char *as = getenv("DMF_ASYNC")) g->async = atoi(as) != 0;
-  if (const char *ss = getenv("DMF_ASYNC_STATIC")) g->async_static = atoi(ss) != 0;
-  if (const char *aw = getenv("DMF_ASYNC_WARPS")) g->async_warps = atoi(aw) > 0 ? (atoi(aw) < WPB ? atoi(aw) : WPB) : 8;
-  if (const char *ba = getenv("DMF_BU_ALPHA")) g->bu_alpha = atoi(ba) > 0 ? atoi(ba) : g->bu_alpha;
-  if (const char *dd = getenv("DMF_DENSE_DIV")) g->dense_div = atoi(dd) > 0 ? atoi(dd) : g->dense_div;
-  if (const char *sl = getenv("DMF_ASYNC_SLEEP_NS")) g->async_sleep_ns = atoi(sl) > 0 ? atoi(sl) : 1024;
-  if (const char *tp = getenv("DMF_ASYNC_TMAX_PEND")) g->async_tmax_pend = atoi(tp) > 0 ? atoi(tp) : 0x7fffffff;
-  if (const char *tm = getenv("DMF_ASYNC_TMAX_US")) g->async_tmax_us = atoll(tm) > 0 ? atoll(tm) : 600;
-  if (const char *bm = getenv("DMF_BUDGET_MUL")) g->budget_mul = atoll(bm) > 0 ? atoll(bm) : 1;
+  {
+    // engine knobs: dmf_options fields (0 = default), each overridable by its DMF_*
+    // environment variable (process-wide; for experiments)
+    const dmf_options &o = g->opt;
+    auto knob = [](int32_t field, const char *env) -> int32_t {
+      const char *e = getenv(env);
+      return e ? (int32_t)atoi(e) : field;
+    };
+    const int32_t sched = knob(o.schedule, "DMF_SCHED");
+    if (sched < 0 || sched > DMF_SCHED_TOPOLOGY) { fail(DMF_EINVAL, "unknown schedule %d", sched); return bail(DMF_EINVAL); }
+    g->async = sched == DMF_SCHED_AUTO || sched == DMF_SCHED_ASYNC;
+    g->async_static = sched == DMF_SCHED_ASYNC;
+    if (const char *as = getenv("DMF_ASYNC")) g->async = atoi(as) != 0;          // legacy switches
+    if (const char *ss = getenv("DMF_ASYNC_STATIC")) g->async_static = atoi(ss) != 0;
+    const int32_t aw = knob(o.async_warps, "DMF_ASYNC_WARPS");
+    g->async_warps = aw > 0 ? (aw < WPB ? aw : WPB) : 8;
+    const int32_t bm = knob(o.budget_mul, "DMF_BUDGET_MUL");
+    g->budget_mul = bm == 0 ? 1 : bm;
+    const int32_t ti = knob(o.tail_items, "DMF_TAIL_ITEMS");
+    g->tail_items = ti == 0 ? 2048 : (ti < 0 ? 0 : ti);
+    g->local_gap = knob(o.local_gap, "DMF_LOCAL_GAP") < 0 ? 0 : 1;
+    g->no_warm = knob(o.warm, "DMF_WARM") < 0;
+    if (const char *nw = getenv("DMF_NO_WARM")) g->no_warm = atoi(nw) != 0;
+    const int32_t td = knob(o.topo_div, "DMF_TOPO_DIV");
+    g->topo_div = sched == DMF_SCHED_TOPOLOGY ? 0x3fffffff : (td == 0 ? 16 : (td < 0 ? 0 : td));
+    g->check_level = knob(o.check_level, "DMF_CHECK_LEVEL");
+    if (const char *ba = getenv("DMF_BU_ALPHA")) g->bu_alpha = atoi(ba) > 0 ? atoi(ba) : g->bu_alpha;
+    if (const char *dd = getenv("DMF_DENSE_DIV")) g->dense_div = atoi(dd) > 0 ? atoi(dd) : g->dense_div;
+    if (const char *sl = getenv("DMF_ASYNC_SLEEP_NS")) g->async_sleep_ns = atoi(sl) > 0 ? atoi(sl) : 1024;
+    for (int i = 0; i < 8; i++)
+      if (o.reserved[i]) { fail(DMF_EINVAL, "dmf_options.reserved must be zero"); return bail(DMF_EINVAL); }
+  }
+  g->chk = (int32_t *)g->alloc(64);
+  g->cnt = (int32_t *)g->alloc(2 * GAPW * sizeof(int32_t));
+  g->cnt_next = (int32_t *)g->alloc(2 * GAPW * sizeof(int32_t));
+  if (!g->cnt || !g->cnt_next || !g->chk) { fail(DMF_ENOMEM, "device allocation failed (level counts)"); return bail(DMF_ENOMEM); }
+  CKB(cudaMemsetAsync(g->cnt, 0, 2 * GAPW * sizeof(int32_t), st));
+  CKB(cudaMemsetAsync(g->cnt_next, 0, 2 * GAPW * sizeof(int32_t), st));
   if (const char *wd = getenv("DMF_WATCHDOG_S")) {
     g->watchdog_s = atof(wd);
     CKB(cudaHostAlloc((void **)&g->hdbg, 64, cudaHostAllocMapped));
@@ -732,6 +856,52 @@ int dmf_export_state(const dmf_graph *g, int64_t *row_ptr, int32_t *dst, int32_t
   if (excess) CK(cudaMemcpyAsync(excess, g->e, (size_t)g->n * 8, cudaMemcpyDefault, st));
   CK(cudaStreamSynchronize(st));
   return DMF_OK;
+}
+
+int dmf_check_state(dmf_graph *g) {
+  g_last_error.clear();
+  if (!g) return fail(DMF_EINVAL, "NULL handle");
+  return check_state(g);
+}
+
+int dmf_import_state(dmf_graph *g, const int32_t *cap, const int32_t *res, const int64_t *excess) {
+  g_last_error.clear();
+  if (!g || !cap || !res || !excess) return fail(DMF_EINVAL, "NULL argument");
+  cudaStream_t st = g->stream;
+  const size_t S4 = (size_t)g->S * 4, n8 = (size_t)g->n * 8;
+  int32_t *tcap = (int32_t *)g->alloc(S4 ? S4 : 4), *tres = (int32_t *)g->alloc(S4 ? S4 : 4);
+  long long *te = (long long *)g->alloc(n8);
+  int rc = DMF_OK;
+  if (!tcap || !tres || !te) rc = fail(DMF_ENOMEM, "device allocation failed (import)");
+  if (rc == DMF_OK) {
+    cudaError_t e = cudaMemcpyAsync(tcap, cap, S4, cudaMemcpyDefault, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(tres, res, S4, cudaMemcpyDefault, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(te, excess, n8, cudaMemcpyDefault, st);
+    if (e != cudaSuccess) rc = fail(DMF_ECUDA, "import copy: %s", cudaGetErrorString(e));
+  }
+  if (rc == DMF_OK) {
+    // capacities of the import: the pair sum 2 needs cap_rev from the same array
+    rc = check_arrays(g, tcap, tres, nullptr, te);
+    if (rc == DMF_ECHECK) { std::string m = g_last_error; rc = fail(DMF_EINVAL, "import rejected: %s", m.c_str()); }
+  }
+  if (rc == DMF_OK) {
+    cudaError_t e = cudaMemcpyAsync(g->cap, tcap, S4, cudaMemcpyDeviceToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(g->res, tres, S4, cudaMemcpyDeviceToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(g->e, te, n8, cudaMemcpyDeviceToDevice, st);
+    if (e == cudaSuccess && g->S) {
+      k_mirror<<<g->grid_blocks > 0 ? g->grid_blocks : 296, 512, 0, st>>>(g->S, g->rev, g->res, g->rres);
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) rc = fail(DMF_ECUDA, "import commit: %s", cudaGetErrorString(e));
+    g->solved = false;       // a valid pseudoflow, not known to be converged
+    g->smin_valid = false;
+    g->warm = false;
+  }
+  if (tcap) g->release(tcap);
+  if (tres) g->release(tres);
+  if (te) g->release(te);
+  return rc;
 }
 
 int dmf_export_labels(const dmf_graph *g, int32_t *hp, int32_t *hm, uint8_t *part, int32_t *rres) {

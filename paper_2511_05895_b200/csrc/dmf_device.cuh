@@ -46,8 +46,13 @@ enum Mode : int32_t {
 enum Stat : int {
   ST_ITERS, ST_LEVELS, ST_BFS_V, ST_BFS_SLOTS, ST_DIS_V, ST_DIS_SLOTS, ST_PUSHES,
   ST_RELABELS, ST_RIE_SLOTS, ST_RIE_SAT, ST_S2_V, ST_S2_ITERS, ST_ROUNDS, ST_ACTIVATIONS, ST_RESET_V, ST_BUDGET_STOPS, ST_BU_LEVELS,
+  ST_GAP_LEVELS, ST_GAP_SKIPS, ST_TOPO_ROUNDS, ST_TAIL_STOPS, ST_S2_SKIP,
   ST_T_PRO, ST_T_RESET, ST_T_BFS, ST_T_DIS, ST_T_RIE, ST_T_EPI, ST_T_BFS_BU, ST_T_BFS_CMP, ST_N
 };
+
+// Local gap (R14 form 2): per-track counts of the vertices at each height h < GAPW.
+// Heights >= GAPW are not counted (no gap is ever reported there).
+constexpr int32_t GAPW = 1024;
 
 // Control block in device memory (zeroed by the host before every launch).
 struct Ctl {
@@ -73,6 +78,12 @@ struct Ctl {
   int32_t ahead;                // next item index to claim (initial worklist first, then the ring)
   int32_t astop;                // work budget spent: stop claiming
   unsigned long long awork;     // discharge work of the phase
+  int32_t atail;                // async: item completions while <= TAIL_PEND items were pending
+  int32_t gtop[2];              // local gap per track: 0 = none, else GAPW - (lowest emptied level)
+  int32_t tact[3];              // topology round r: some vertex became (or stayed) active [r % 3]
+  int32_t check;                // invariant check: first violated check (0 = none) and a witness
+  int32_t check_at;
+  int32_t pdef, pexc;           // DYN_PP: deficit / excess vertices in P (stage 2 / P-reach skip)
 };
 
 // Everything a kernel needs, passed by value.  Slot arrays are SoA int32[S]:
@@ -110,13 +121,16 @@ struct Dev {
   int32_t aq_mask;
   int32_t async;             // 1: asynchronous discharge phase, 0: barrier-separated rounds
   int32_t async_warps;       // consumer warps per CTA in the asynchronous phase
-  long long async_tmax_ns;   // time budget of one asynchronous phase (then a global relabel)
   int32_t static_pp;         // MODE_STATIC: static push-pull initialisation (also saturate t's in-edges)
   int32_t bu_alpha;          // BFS: bottom-up when frontier slots x bu_alpha > unvisited slots (BU_ALPHA)
   int32_t dense_div;         // BFS: top-down by stores + compaction when frontier slots x dense_div >= S (DENSE_DIV)
   int32_t async_sleep_ns;    // back-off of a warp waiting for a ring item
-  int32_t async_tmax_pend;   // repairs: the time budget stops a phase only while <= this many items are pending
-  int32_t async_tmax_any;    // 1: the time budget applies however much work is pending (repairs)
+  int32_t *cnt;              // local gap: [2 tracks][GAPW] vertices per height (this call)
+  int32_t *cnt_next;         // DYN_PP: the final labels' histogram for the next call's warm start
+  int32_t local_gap;         // 1: local gap exit on (R14 form 2)
+  int32_t topo_div;          // topology-driven phase when > n / topo_div vertices are active (0: never)
+  int32_t tail_items;        // async progress stop (<= 0: off)
+  int32_t check_level;
   int32_t *plist;            // region P of push-pull stage 2
   int32_t *stamp;            // per-slot batch stamp (duplicate detection)
   const int32_t *bu, *bv, *bc;  // batch entries

@@ -44,6 +44,7 @@ constexpr int SW = 256;             // staged entries per worklist bin (bins 0..
 struct Stage {
   int32_t cnt[6];                   // 0,1: frontier bins 0,1; 2..5: worklist bins 0..3
   int32_t base[6];
+  int32_t lv[2];                    // vertices labelled in this phase per track (local-gap level counts)
   int32_t f[2][SF];
   int32_t w[4][SW];
 };
@@ -66,7 +67,10 @@ struct Smem {
   int32_t wcc[WPB];                // async discharge: per-warp candidate counts (warp w: cand[w*WCAP..])
   int32_t astop;                   // async discharge: this CTA has seen ctl->astop
   unsigned long long apoll;        // async discharge: last global poll of ctl->astop
-  unsigned long long astart;       // async discharge: this CTA's phase start (time budget)
+  int32_t amode;                   // current discharge phase: 1 = asynchronous ring, 0 = rounds / topology
+  int32_t topo;                    // current discharge phase is topology-driven
+  int32_t tslot;                   // topology round r: activity flag ctl->tact[r % 3]
+  int32_t lvcnt[2];                // BFS: vertices labelled by this CTA in the current level, per track
   int32_t cand[2048];
   Stage st;                    // block-staged appends (BFS)
   TileSm ts;                   // tiled compaction (dense top-down BFS levels)
@@ -100,6 +104,33 @@ __device__ __forceinline__ Track make_track(const Dev &d, int tr) {
 
 __device__ __forceinline__ void sstat_add(Smem &sm, int which, unsigned long long x) {
   if (x) atomicAdd(&sm.stat[which], x);
+}
+
+// ---------------------------------------------------------------------------
+// Local gap (R14 form 2; the gap heuristic of P:114).  cnt[tr][h] counts the vertices
+// of track tr's region at height h < GAPW: the BFS adds each labelled vertex to its
+// level, a lift moves u from its old height to the new one.  When a lift empties a
+// level g, no vertex above g can reach a root of the track any more (a residual path
+// descends at most one level per edge under a valid labelling, so it would cross g),
+// and every vertex above the lowest emptied level stops discharging for the rest of
+// the phase WITHOUT writing its height: RIE and the next fresh BFS (R9) see the same
+// state as without the heuristic.  A count that is transiently wrong under races can
+// only stop a vertex that could still reach a root; it stays active and the fresh BFS
+// re-collects it, so the heuristic never changes a result, only the work.
+__device__ __forceinline__ int32_t gap_limit(const Dev &d, int tr) {
+  if (!d.local_gap) return 0x7fffffff;
+  const int32_t g = *(const volatile int32_t *)&d.ctl->gtop[tr];
+  return g ? GAPW - g : 0x7fffffff;
+}
+// u of track tr moves from height `from` (< |V|) to `to` (<= |V|)
+__device__ __forceinline__ void gap_move(const Dev &d, Smem &sm, int tr, int32_t from, int32_t to) {
+  if (!d.local_gap) return;
+  int32_t *c = d.cnt + tr * GAPW;
+  if (to < GAPW && to < d.n) atomicAdd(c + to, 1);          // arrive first: u itself never leaves a false gap
+  if (from < GAPW && atomicSub(c + from, 1) == 1 && from > 0) {
+    atomicMax(&d.ctl->gtop[tr], GAPW - from);
+    sstat_add(sm, ST_GAP_LEVELS, 1);
+  }
 }
 
 __device__ void PhaseClock::lap(const Dev &d, Smem &sm, int which, int32_t it, int32_t sub, int32_t items,
@@ -335,9 +366,14 @@ __device__ __forceinline__ void async_enqueue(const Dev &d, int32_t v, uint32_t 
 __device__ __forceinline__ void activate(const Dev &d, const Track &k, const BL &nxt, int32_t v, uint32_t tag,
                                          Smem &sm, bool ring = true) {
   if (v == d.s || v == d.t) return;
+  if (sm.topo) {                                    // topology-driven: the next sweep finds v itself
+    sstat_add(sm, ST_ACTIVATIONS, 1);
+    d.ctl->tact[sm.tslot] = 1;
+    return;
+  }
   if (atomicCAS(d.inq + v, 0, 1) != 0) return;     // (a vertex at height >= |V| exits at once)
   sstat_add(sm, ST_ACTIVATIONS, 1);
-  if (d.async && ring) { async_enqueue(d, v, tag); return; }
+  if (sm.amode && ring) { async_enqueue(d, v, tag); return; }
   const int32_t pos = atomicAdd(&sm.acnt, 1);
   if (pos < ACAP) act_buf(sm)[pos] = (int32_t)((uint32_t)v | tag);
   else bl_append_one(d, nxt, v, tag);
@@ -367,10 +403,10 @@ __device__ __forceinline__ void push_slot(const Dev &d, const Track &k, const BL
   // rounds: one list per CTA, checked at the round end; async: one list per warp,
   // checked after the warp's item (async_candidates)
   const int w = (int)(threadIdx.x >> 5);
-  const int32_t pos = d.async ? atomicAdd(&sm.wcc[w], 1) : atomicAdd(&sm.ccnt, 1);
-  if (pos < (d.async ? WCAP : CCAP)) {
+  const int32_t pos = sm.amode ? atomicAdd(&sm.wcc[w], 1) : atomicAdd(&sm.ccnt, 1);
+  if (pos < (sm.amode ? WCAP : CCAP)) {
     atom_add(d.e + v, (long long)take * k.sign);                           // e(v) += d
-    sm.cand[d.async ? w * WCAP + pos : pos] = (int32_t)((uint32_t)v | tag);
+    sm.cand[sm.amode ? w * WCAP + pos : pos] = (int32_t)((uint32_t)v | tag);
   } else {
     const long long eo = (long long)atomicAdd(reinterpret_cast<unsigned long long *>(d.e + v),
                                               (unsigned long long)((long long)take * k.sign)) * k.sign;
@@ -400,6 +436,7 @@ constexpr int TILE_ITEMS = 4;                     // vertices per thread per com
 
 struct BfsCtx {
   int32_t lvl;
+  int32_t tgt;                      // height the vertices labelled in this phase receive (lvl + 1; 0 in RESET)
   bool collect;
   uint32_t bu;                      // bit tr: bottom-up this level on track tr
   uint32_t dense;                   // bit tr: top-down by idempotent stores + compaction
@@ -514,6 +551,16 @@ __device__ __forceinline__ void claim_push(const Dev &d, Stage &st, const BfsCtx
     chunks_conv(c.wl, wb >= 2, deg, v, tr ? TRACK_BIT : 0u);   // big rows: chunked discharge
   }
   if (claimed) fs.add(tr, deg);
+  if (d.local_gap) {                // level counts of the local gap (R14 form 2)
+    const unsigned m = __ballot_sync(0xffffffffu, claimed);
+    if (m) {
+      const unsigned m1 = __ballot_sync(0xffffffffu, claimed && tr);
+      if ((threadIdx.x & 31) == 0) {
+        if (m & ~m1) atomicAdd(&st.lv[0], __popc(m & ~m1));
+        if (m1) atomicAdd(&st.lv[1], __popc(m1));
+      }
+    }
+  }
 }
 
 // single-thread version (bottom-up pass B leaders)
@@ -539,6 +586,7 @@ __device__ __forceinline__ void claim_one(const Dev &d, Stage &st, const BfsCtx 
     }
   }
   fs.add(tr, deg);
+  if (d.local_gap) atomicAdd(&st.lv[tr], 1);
 }
 
 __device__ __forceinline__ bool activity(const Dev &d, bool collect, int tr, int32_t v) {
@@ -751,7 +799,7 @@ __device__ __forceinline__ void bfs_bottom_up_b(const Dev &d, const G &g, Smem &
 template <class Classify>
 __device__ __forceinline__ void compact_domain(const Dev &d, TileSm &ts, int32_t N, const int32_t *dom,
                                                const BL &next, const BL &wl, bool collect, Classify classify,
-                                               long long &fs0, long long &fs1) {
+                                               long long &fs0, long long &fs1, int32_t &nv0, int32_t &nv1) {
   const int lane = threadIdx.x & 31;
   const int32_t tile_sz = TILE_ITEMS * NT;
   WarpG g{lane};
@@ -777,7 +825,7 @@ __device__ __forceinline__ void compact_domain(const Dev &d, TileSm &ts, int32_t
       const int fb = front ? (deg <= BIN0_MAX ? 0 : (deg <= BIN1_MAX ? 1 : 2)) : -1;
       const int wb = (collect && act) ? (deg <= BIN0_MAX ? 0 : (deg <= BIN1_MAX ? 1 : 2)) : -1;
       if (wb >= 0) d.inq[v] = 1;
-      if (front) { if (tr) fs1 += deg; else fs0 += deg; }
+      if (front) { if (tr) { fs1 += deg; nv1++; } else { fs0 += deg; nv0++; } }
       vv[j] = v; fc[j] = (int8_t)fb; wc[j] = (int8_t)wb; tg[j] = tr ? TRACK_BIT : 0u;
       fo[j] = 0; wo[j] = 0;
       // frontier bins 0/1: ballot per bin
@@ -908,14 +956,20 @@ __device__ __forceinline__ void dis_flush(const Dev &d, Smem &sm, const BL &nxt,
   vflush(d, sm.ts, rel_buf(sm), r, rl);
 }
 
-// block-wide: flush the stages and publish the per-CTA frontier slot sums
-__device__ __forceinline__ void bfs_flush(Smem &sm, Stage &st, const BfsCtx &c, FS &fs) {
+// block-wide: flush the stages and publish the per-CTA frontier slot sums and the
+// level counts of the vertices labelled in this phase
+__device__ __forceinline__ void bfs_flush(const Dev &d, Smem &sm, Stage &st, const BfsCtx &c, FS &fs) {
   stage_flush(st, c.next, c.wl);
   BlockG bg{sm.red};
   const long long f0 = bg.sum(fs.a), f1 = bg.sum(fs.b);
   if (threadIdx.x == 0) {
     if (f0) atomicAdd(c.fs_next, (unsigned long long)f0);
     if (f1) atomicAdd(c.fs_next + 1, (unsigned long long)f1);
+    if (c.tgt < GAPW && c.tgt < d.n) {
+      if (st.lv[0]) atomicAdd(d.cnt + c.tgt, st.lv[0]);
+      if (st.lv[1]) atomicAdd(d.cnt + GAPW + c.tgt, st.lv[1]);
+    }
+    st.lv[0] = 0; st.lv[1] = 0;
   }
 }
 
@@ -933,7 +987,7 @@ __device__ __forceinline__ void bfs_expand_level(const Dev &d, cg::grid_group &g
     const int32_t *b0 = cur.bin(0);
     for (int32_t x = gw * 32; x < c[0]; x += nw * 32) td_small_chunk(d, sm, st, b0, x, min(32, c[0] - x), ctx, fs);
   }
-  bfs_flush(sm, st, ctx, fs);
+  bfs_flush(d, sm, st, ctx, fs);
   gsync(d, grid, sm);
   clk.lap(d, sm, ST_T_BFS, it, ctx.lvl, total(c), (int32_t)ctx.bu | (c[3] << 3));
   if (bu) {
@@ -950,7 +1004,7 @@ __device__ __forceinline__ void bfs_expand_level(const Dev &d, cg::grid_group &g
         const int32_t gw = blockIdx.x * WPB + (threadIdx.x >> 5), nw = gridDim.x * WPB;
         for (int32_t x = gw; x < q1; x += nw) bfs_bottom_up_b(d, g, sm, st, ctx, bul[x], fs);
       }
-      bfs_flush(sm, st, ctx, fs);
+      bfs_flush(d, sm, st, ctx, fs);
       gsync(d, grid, sm);
       clk.lap(d, sm, ST_T_BFS_BU, it, ctx.lvl, q1 + q2, q2);
     }
@@ -984,7 +1038,7 @@ __device__ __forceinline__ void discharge(const Dev &d, const G &g, Smem &sm, in
   // u for the next round.  async: u keeps the flag while it is being discharged (no
   // second warp may take u concurrently: both would push the same residual) and the
   // epilogue below clears it and re-checks e(u).
-  if (!d.async && g.rank() == 0) { d.inq[u] = 0; __threadfence(); }
+  if (!sm.amode && g.rank() == 0) { d.inq[u] = 0; __threadfence(); }
   const unsigned long long t_start = d.trace ? gtimer() : 0;
 #ifdef DMF_DEBUG_BUSY
   if (g.rank() == 0 && atomicExch(d.dcnt + u, 1) != 0) atomicCAS(&d.ctl->pad, 0, u + 1);
@@ -994,8 +1048,12 @@ __device__ __forceinline__ void discharge(const Dev &d, const G &g, Smem &sm, in
   bool relabelled = false;
   unsigned long long scanned = 0, pushes = 0, lifts = 0;
   long long eu = 0;
-  if (g.rank() == 0) eu = ldv(d.e + u) * k.sign;
+  int32_t glim = 0x7fffffff;          // local gap: heights above this stop (R14 form 2)
+  if (g.rank() == 0) { eu = ldv(d.e + u) * k.sign; glim = gap_limit(d, tr); }
   eu = g.bcast(eu);
+  glim = (int32_t)g.bcast(glim);
+  const bool gapped = hu < n && hu > glim && eu > 0;
+  if (gapped) eu = 0;                 // above an emptied level: cannot reach a root this phase
   int cyc = 0;
   long long *bud = G::size == 1 ? nullptr
                   : (G::size == NT ? &sm.budget[4 * WPB]
@@ -1067,13 +1125,19 @@ __device__ __forceinline__ void discharge(const Dev &d, const G &g, Smem &sm, in
     nmin = g.min(nmin);                      // every admissible slot saturated: lift
     const int32_t nh = nmin == ~0ull ? n : (int32_t)min((unsigned long long)n, nmin + 1);
     if (nh > hu) {
+      if (g.rank() == 0) {
+        k.hgt[u] = nh;
+        gap_move(d, sm, tr, hu, nh);
+        glim = gap_limit(d, tr);
+      }
       hu = nh;
-      if (g.rank() == 0) k.hgt[u] = hu;
       relabelled = true;
       lifts++;
+      glim = (int32_t)g.bcast(glim);
+      if (hu < n && hu > glim) { eu = 0; break; }   // lifted above an emptied level: stop
     }
   }
-  if (d.async) {                        // every member's pushes land before u is released
+  if (sm.amode) {                       // every member's pushes land before u is released
     if (pushes > 0) __threadfence();
     g.sync();
   }
@@ -1089,11 +1153,13 @@ __device__ __forceinline__ void discharge(const Dev &d, const G &g, Smem &sm, in
     if (atomicExch(d.dcnt + u, 0) != 1) atomicCAS(&d.ctl->pad, 0, -(u + 1));
     __threadfence();
 #endif
-    if (d.async) {
+    const bool stopped = gapped || (hu < n && hu > glim);   // local gap: not re-queued this phase
+    if (stopped) sstat_add(sm, ST_GAP_SKIPS, 1);
+    if (sm.amode) {
       atomicExch(d.inq + u, 0);
       __threadfence();
-      if (hu < n && ldv(d.e + u) * k.sign > 0) activate(d, k, nxt, u, tag, sm);
-    } else if (cyc == d.kc && hu < n && eu > 0) {
+      if (!stopped && hu < n && ldv(d.e + u) * k.sign > 0) activate(d, k, nxt, u, tag, sm);
+    } else if (!stopped && cyc == d.kc && hu < n && eu > 0) {
       activate(d, k, nxt, u, tag, sm);  // KERNELCYCLES spent
     }
     if (relabelled && d.rlf[u] == 0) { d.rlf[u] = 1; stage_relabelled(d, rl, u, tag, sm); }
@@ -1142,10 +1208,12 @@ __device__ __forceinline__ void discharge_chunk(const Dev &d, Smem &sm, long lon
   WarpG g{lane};
   // excess already claimed by the other chunks (or drained): nothing to push here,
   // and an admissible slot may remain -> no lift (dry); skips the slot loads
+  int32_t glim = 0x7fffffff;             // local gap (R14 form 2)
   if (hu < n) {
     long long e0 = 0;
-    if (lane == 0) e0 = ldv(d.e + u) * k.sign;
-    dry = g.bcast(e0) <= 0;
+    if (lane == 0) { e0 = ldv(d.e + u) * k.sign; glim = gap_limit(d, tr); }
+    glim = (int32_t)g.bcast(glim);
+    dry = g.bcast(e0) <= 0 || hu > glim;  // above an emptied level: no pushes, and no lift below
   }
   if (hu < n && !dry) {
     for (int32_t b0 = beg; b0 < end; b0 += 128) {   // warp-uniform trip count (collectives inside)
@@ -1212,15 +1280,19 @@ __device__ __forceinline__ void discharge_chunk(const Dev &d, Smem &sm, long lon
       atomicExch(d.inq + u, 0);
       __threadfence();
       const long long eu = ldv(d.e + u) * k.sign;
-      if (eu > 0 && hu < n) {
+      if (eu > 0 && hu < n && hu > glim) {
+        sstat_add(sm, ST_GAP_SKIPS, 1);      // above an emptied level: parked until the fresh BFS
+      } else if (eu > 0 && hu < n) {
         int32_t nh = hu;
         if (mn >= hu) nh = mn >= n ? n : mn + 1;   // every residual slot at >= h(u): lift
         if (nh > hu) {
           k.hgt[u] = nh;
+          gap_move(d, sm, tr, hu, nh);
           lifts = 1;
           if (d.rlf[u] == 0) { d.rlf[u] = 1; stage_relabelled(d, rl, u, tag, sm); }
         }
-        if (nh < n) activate(d, k, nxt, u, tag, sm);
+        if (nh < n && nh <= gap_limit(d, tr)) activate(d, k, nxt, u, tag, sm);
+        else if (nh < n) sstat_add(sm, ST_GAP_SKIPS, 1);
       }
       sstat_add(sm, ST_DIS_V, 1);
       sstat_add(sm, ST_RELABELS, lifts);
@@ -1364,6 +1436,7 @@ __device__ __forceinline__ void rie_chunks(const Dev &d, Smem &sm, const long lo
 // astop.  Waiting warps poll their ring slot and, at most once per ~1 us per CTA, the
 // flag (through shared memory).  Items left behind by a budget stop are swept (their
 // inq flags cleared) by async_sweep; the next fresh BFS re-collects them (R9).
+constexpr uint32_t TAIL_PEND = 64;       // async: "tail" = at most this many items pending
 __device__ __forceinline__ long long ldvol(const long long *p) { return *(const volatile long long *)p; }
 __device__ __forceinline__ int32_t ldvol(const int32_t *p) { return *(const volatile int32_t *)p; }
 
@@ -1429,14 +1502,15 @@ __device__ __forceinline__ void async_phase(const Dev &d, Smem &sm, const BL &in
     if (lane == 0) {
       const unsigned long long old = atomicAdd(&ctl->aw, ~0ull);        // item done (after its enqueues)
       bool stop = (uint32_t)old == 1u;                                    // nothing left anywhere
-      // time budget: a long phase means excess creeping up one lift at a time on stale
-      // heights (a ping-pong the rounds bounded by charging every round); a global
-      // relabel fixes every height at once
-      // (a repair after a batch: always; the static solve from zero flow: only while
-      // little is pending -- a long phase with plenty of parallel work is useful there)
-      if (!stop && (uint32_t)old <= (uint32_t)(d.async_tmax_any ? d.async_tmax_pend : 64) &&
-          gtimer() - sm.astart > (unsigned long long)d.async_tmax_ns)
+      // progress stop: a long low-parallelism tail means excess creeping up one lift at a
+      // time on stale heights (a ping-pong the rounds bound by charging every round); one
+      // global relabel fixes every height at once.  Counted in items, not time, so the
+      // work done does not depend on the clock or the box.
+      if (!stop && d.tail_items > 0 && (uint32_t)old <= (uint32_t)TAIL_PEND &&
+          atomicAdd(&ctl->atail, 1) + 1 >= d.tail_items) {
         stop = true;
+        sstat_add(sm, ST_TAIL_STOPS, 1);
+      }
       if (!stop && sm.work > 32768ull) {                                  // budget: flushed in 32K-slot units
         const unsigned long long w = atomicExch(&sm.work, 0ull);
         stop = (long long)(atomicAdd(&ctl->awork, w) + w) > d.work_budget;
@@ -1495,6 +1569,47 @@ struct Lists {      // (members, not arrays: a dynamically indexed array would l
 };
 
 
+// Topology-driven sweep: every vertex of the domain is tested
+// (thread per vertex, "idle when inactive") and an active one is discharged in place:
+// by its own thread (<= BIN0_MAX slots), by its warp (<= BIN1_MAX), or queued as
+// CH-slot chunks for the grid after the sweep.  No worklist is built: the next sweep
+// finds the vertices that became active (activate() only raises ctl->tact).
+__device__ __forceinline__ void topology_sweep(const Dev &d, Smem &sm, const int32_t *dom, int32_t N, bool use0,
+                                               bool use1, const BL &rl, const BL &tch) {
+  const int lane = threadIdx.x & 31;
+  const int32_t nt = gridDim.x * NT, n = d.n;
+  WarpG wg{lane};
+  for (int32_t b = blockIdx.x * NT + (threadIdx.x & ~31); b < N; b += nt) {
+    const int32_t x = b + lane;
+    int32_t v = 0, deg = 0, entry = 0;
+    bool act = false;
+    if (x < N) {
+      v = dom ? dom[x] : x;
+      if (ldv(d.inq + v)) d.inq[v] = 0;        // worklist flag of the BFS collection: unused here
+      if (v != d.s && v != d.t) {
+        const long long ev = ldv(d.e + v);
+        int tr = -1;
+        if (use0 && ev > 0 && ldv(d.hp + v) < n) tr = 0;
+        else if (use1 && ev < 0 && ldv(d.hm + v) < n) tr = 1;
+        if (tr >= 0) {
+          deg = d.row[v + 1] - d.row[v];
+          act = deg > 0;
+          entry = (int32_t)((uint32_t)v | (tr ? TRACK_BIT : 0u));
+        }
+      }
+    }
+    chunks_conv(tch, act && deg > BIN1_MAX, deg, v, (uint32_t)entry & TRACK_BIT);
+    if (act && deg <= BIN0_MAX) discharge(d, ThreadG{}, sm, entry, rl, tch, nullptr);
+    __syncwarp();
+    unsigned m = __ballot_sync(0xffffffffu, act && deg > BIN0_MAX && deg <= BIN1_MAX);
+    while (m) {
+      const int j = __ffs(m) - 1;
+      m &= m - 1;
+      discharge(d, wg, sm, __shfl_sync(0xffffffffu, entry, j), rl, tch, nullptr);
+    }
+  }
+}
+
 // The device loop: repeat { RESET; BFS levels (+ worklist); if no active: stop;
 //                           rounds of { DISCHARGE; RIE } until no vertex is queued }.
 // Counter discipline (each counter is zeroed by block 0 in a phase where nobody
@@ -1528,7 +1643,7 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
    if (!(warm && iter == 0)) {
     // ---------------- RESET: heights of the domain, roots -> frontier level 0
     if (blockIdx.x == 0 && threadIdx.x < NB) {
-      if (threadIdx.x == 0) { ctl->aw = 0; ctl->ahead = 0; ctl->astop = 0; ctl->awork = 0; }
+      if (threadIdx.x == 0) { ctl->aw = 0; ctl->ahead = 0; ctl->astop = 0; ctl->awork = 0; ctl->atail = 0; }
       rlc[threadIdx.x] = 0;
       qc[NB + threadIdx.x] = 0;
       if (threadIdx.x < 3) ctl->work[threadIdx.x] = 0;
@@ -1539,7 +1654,7 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
       // heights: 0 for roots, |V| for the rest of the track's region, |V|+1 outside it
       FS fs;
       long long mu0 = 0, mu1 = 0;
-      const BfsCtx c0{0, false, 0u, 0u, BL{L.q0, qc, n, L.qc0},
+      const BfsCtx c0{0, 0, false, 0u, 0u, BL{L.q0, qc, n, L.qc0},
                       BL{L.wl0, wlc, n, L.cw0}, ctl->fs};
       for (int32_t b = blockIdx.x * NT + (threadIdx.x & ~31); b < N; b += nt) {
         const int32_t x = b + (threadIdx.x & 31);
@@ -1588,7 +1703,7 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
         }
         claim_push(d, sm.st, c0, r0 || r1, false, v, r1 ? 1 : 0, fs);
       }
-      bfs_flush(sm, sm.st, c0, fs);
+      bfs_flush(d, sm, sm.st, c0, fs);
       BlockG bg{sm.red};
       mu0 = bg.sum(mu0); mu1 = bg.sum(mu1);
       if (threadIdx.x == 0) {
@@ -1628,7 +1743,7 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
       const bool bu1 = f1 > 0 && (unsigned long long)f1 * d.bu_alpha > (unsigned long long)(mu[1] > 0 ? mu[1] : 0);
       const bool dn0 = !bu0 && f0 > 0 && (unsigned long long)f0 * d.dense_div >= (unsigned long long)d.S;
       const bool dn1 = !bu1 && f1 > 0 && (unsigned long long)f1 * d.dense_div >= (unsigned long long)d.S;
-      const BfsCtx ctx{lvl, collect, (bu0 ? 1u : 0u) | (bu1 ? 2u : 0u), (dn0 ? 1u : 0u) | (dn1 ? 2u : 0u),
+      const BfsCtx ctx{lvl, lvl + 1, collect, (bu0 ? 1u : 0u) | (bu1 ? 2u : 0u), (dn0 ? 1u : 0u) | (dn1 ? 2u : 0u),
                        BL{L.q((lvl + 1) & 1), qc + NB * ((lvl + 1) % 3), n, L.qc((lvl + 1) & 1)},
                        BL{L.wl0, wlc, n, L.cw0}, ctl->fs + 2 * ((lvl + 1) % 3)};
       if (lead && (bu0 || bu1)) sstat_add(sm, ST_BU_LEVELS, 1);
@@ -1636,17 +1751,23 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
                        ctl->bulc + 2 * (lvl & 1));
       if (dn0 || dn1) {                             // dense top-down tracks: build lvl+1 by compaction
         long long g0 = 0, g1 = 0;
+        int32_t v0 = 0, v1 = 0;
         compact_domain(d, sm.ts, N, on_plist ? d.plist : nullptr, ctx.next, ctx.wl, collect,
           [&](int32_t v, int &tr, bool &front, bool &act) {
             if (dn0 && ldv(d.hp + v) == lvl + 1) { tr = 0; front = true; }
             else if (dn1 && ldv(d.hm + v) == lvl + 1) { tr = 1; front = true; }
             if (front) act = activity(d, collect, tr, v);
-          }, g0, g1);
+          }, g0, g1, v0, v1);
         BlockG bg{sm.red};
         g0 = bg.sum(g0); g1 = bg.sum(g1);
+        const long long nv0 = bg.sum(v0), nv1 = bg.sum(v1);
         if (threadIdx.x == 0) {
           if (g0) atomicAdd(ctx.fs_next, (unsigned long long)g0);
           if (g1) atomicAdd(ctx.fs_next + 1, (unsigned long long)g1);
+          if (d.local_gap && lvl + 1 < GAPW && lvl + 1 < n) {     // dense levels: counted here, once per vertex
+            if (nv0) atomicAdd(d.cnt + lvl + 1, (int32_t)nv0);
+            if (nv1) atomicAdd(d.cnt + GAPW + lvl + 1, (int32_t)nv1);
+          }
         }
         gsync(d, grid, sm);
         clk.lap(d, sm, ST_T_BFS_CMP, iter, lvl, N);
@@ -1667,19 +1788,60 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
       if (lead) ctl->status = -8;                // DMF_ENOCONV
       break;
     }
-    // ---------------- rounds of DISCHARGE (push || pull tracks), then RIE once
-    // (Alg.1 l.168-169: PushRelabel, then RemoveInvalidEdges, then the next BFS)
+    // ---------------- DISCHARGE (push || pull tracks), then RIE once
+    // (Alg.1 l.168-169: PushRelabel, then RemoveInvalidEdges, then the next BFS).
+    // Schedule of the phase: topology-driven sweeps when many vertices are
+    // active (the auto-switch of P:923), else the data-driven worklist as an
+    // asynchronous ring or as barrier-separated rounds.
     unsigned long long spent = 0;                 // work since the global relabel (same in every thread)
     const BL rl{L.rl, rlc, n, L.rlc};
     int32_t w_async[NB];
-    if (d.async) cta_counts(sm, wlc, w_async);
-    if (d.async && total(w_async) > 0) {
+    cta_counts(sm, wlc, w_async);
+    const int32_t ndom = on_plist ? cta_ld(sm, &ctl->pcnt) : n;
+    const bool topo = d.topo_div > 0 && (long long)total(w_async) * d.topo_div > (long long)ndom;
+    if (threadIdx.x == 0) { sm.amode = d.async && !topo; sm.topo = topo; }
+    __syncthreads();
+    if (topo) {
+      for (int r = 0;; ++r) {
+        // rings of 3 as in the rounds below, shifted by one: slot 0 of wlc holds the BFS
+        // worklist counts (unused here) when round 0 starts
+        const int cur = (r + 1) % 3, nx = (r + 2) % 3, nn = r % 3;
+        if (threadIdx.x == 0) sm.tslot = cur;
+        if (blockIdx.x == 0 && threadIdx.x < NB) {
+          wlc[NB * nn + threadIdx.x] = 0;         // (same ring discipline as the rounds below)
+          if (threadIdx.x == 0) { ctl->tact[nx] = 0; ctl->work[nx] = 0; }
+        }
+        __syncthreads();
+        const BL tch{L.wl1, wlc + NB * cur, n, L.cw1};   // chunks of the big active vertices of this sweep
+        topology_sweep(d, sm, on_plist ? d.plist : nullptr, ndom, use0, use1, rl, tch);
+        dis_flush(d, sm, tch, rl);
+        gsync(d, grid, sm);
+        {
+          const int32_t nc = cta_ld(sm, wlc + NB * cur + 3);
+          const int32_t gw = blockIdx.x * WPB + (threadIdx.x >> 5), nw = gridDim.x * WPB;
+          for (int32_t x = gw; x < nc; x += nw) discharge_chunk(d, sm, tch.cq[x], rl, tch);
+          dis_flush(d, sm, tch, rl);
+        }
+        if (threadIdx.x == 0 && sm.work) { atomicAdd(ctl->work + cur, sm.work); sm.work = 0; }
+        if (lead) { sstat_add(sm, ST_ROUNDS, 1); sstat_add(sm, ST_TOPO_ROUNDS, 1); }
+        gsync(d, grid, sm);
+        clk.lap(d, sm, ST_T_DIS, iter, r, ndom, 0);
+        cta_snap(sm, 2, [&](int k) {
+          return k == 0 ? (long long)ldv(ctl->tact + cur) : ldv(reinterpret_cast<const long long *>(ctl->work + cur));
+        });
+        spent += (unsigned long long)sm.cv[1] + (unsigned long long)(d.S >> 4);
+        if (sm.cv[0] == 0) break;                 // no vertex became or stayed active
+        if (r + 1 >= MAX_ROUNDS || (long long)spent > d.work_budget) {
+          if (lead) sstat_add(sm, ST_BUDGET_STOPS, 1);
+          break;
+        }
+      }
+      if (threadIdx.x == 0) sm.topo = 0;
+    } else if (d.async && total(w_async) > 0) {
       const int32_t *w = w_async;
       if (lead) ctl->aw = (unsigned long long)total(w);   // (tail 0) published by the barrier below
       if (threadIdx.x == 0) { sm.astop = 0; sm.apoll = 0; }
       gsync(d, grid, sm);
-      if (threadIdx.x == 0) sm.astart = gtimer();
-      __syncthreads();
       const BL init{L.wl0, wlc, n, L.cw0};
       async_phase(d, sm, init, w, rl, BL{L.wl1, wlc + NB, n, L.cw1});
       dis_flush(d, sm, BL{L.wl1, wlc + NB, n, L.cw1}, rl);
@@ -1690,7 +1852,7 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
       const bool stopped = async_sweep(d, sm, init, w);
       if (lead && stopped) sstat_add(sm, ST_BUDGET_STOPS, 1);
     }
-    for (int r = 0; !d.async; ++r) {
+    for (int r = 0; !d.async && !topo; ++r) {
       // wlc / work rings of 3: round r reads [r%3], fills [(r+1)%3]; a slot is zeroed
       // only when every block has passed the barrier after its last read
       const int cur = r % 3, nx = (r + 1) % 3, nn = (r + 2) % 3;
@@ -1740,8 +1902,10 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
       for (int q = 0; q < 3; q++) wlc[NB * q + threadIdx.x] = 0;
       if (threadIdx.x < 3) for (int q = 0; q < 3; q++) ctl->claim[3 * q + threadIdx.x] = 0;
       qc[threadIdx.x] = 0;                        // for the next RESET
-      if (threadIdx.x < 2) { ctl->fs[threadIdx.x] = 0; ctl->mu[threadIdx.x] = 0; }
+      if (threadIdx.x < 2) { ctl->fs[threadIdx.x] = 0; ctl->mu[threadIdx.x] = 0; ctl->gtop[threadIdx.x] = 0; }
     }
+    if (blockIdx.x == 0 && d.local_gap)           // level counts: rebuilt by the next RESET + BFS
+      for (int i = threadIdx.x; i < 2 * GAPW; i += NT) d.cnt[i] = 0;
     {
       int32_t rc[NB];
       cta_counts(sm, rlc, rc);
@@ -1789,8 +1953,16 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(const __grid_con
   __shared__ Smem sm;
   for (int i = threadIdx.x; i < ST_N; i += NTHREADS) sm.stat[i] = 0;
   if (threadIdx.x < 6) sm.st.cnt[threadIdx.x] = 0;
-  if (threadIdx.x == 0) { sm.work = 0; sm.tprev = gtimer(); sm.acnt = 0; sm.rcnt = 0; sm.ccnt = 0; sm.astop = 0; sm.apoll = 0; }
+  if (threadIdx.x == 0) { sm.work = 0; sm.tprev = gtimer(); sm.acnt = 0; sm.rcnt = 0; sm.ccnt = 0; sm.astop = 0; sm.apoll = 0;
+                          sm.amode = 0; sm.topo = 0; sm.tslot = 0; sm.st.lv[0] = 0; sm.st.lv[1] = 0; }
   if (threadIdx.x < WPB) sm.wcc[threadIdx.x] = 0;
+  if (blockIdx.x == 0 && d.local_gap) {
+    // level counts of the local gap: a DYN_PP warm start keeps the previous call's
+    // (the final labels' histogram, see the PP epilogue); every other call rebuilds
+    // them from its first RESET.  Published by the first grid barrier.
+    if (!(mode == MODE_PP && d.warm)) for (int i = threadIdx.x; i < 2 * GAPW; i += NTHREADS) d.cnt[i] = 0;
+    if (mode == MODE_PP) for (int i = threadIdx.x; i < 2 * GAPW; i += NTHREADS) d.cnt_next[i] = 0;
+  }
   __syncthreads();
   const int32_t n = d.n;
   const int32_t gt = blockIdx.x * NTHREADS + threadIdx.x, nt = gridDim.x * NTHREADS;
@@ -1879,11 +2051,15 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(const __grid_con
         const uint8_t p = ldv(d.part + x);
         const long long ev = ldv(d.e + x);
         if (p == PART_T) {
-          if (ev < 0) d.hp[x] = 0;
-          else if (ev > 0 && ldv(d.hp + x) < n) activate(d, make_track(d, 0), wl0, x, 0u, sm, false);
+          if (ev < 0) {
+            const int32_t old = atomicExch(d.hp + x, 0);          // (x may be named by several entries)
+            if (old != 0 && old < n) gap_move(d, sm, 0, old, 0);
+          } else if (ev > 0 && ldv(d.hp + x) < n) activate(d, make_track(d, 0), wl0, x, 0u, sm, false);
         } else if (p == PART_S) {
-          if (ev > 0) d.hm[x] = 0;
-          else if (ev < 0 && ldv(d.hm + x) < n) activate(d, make_track(d, 1), wl0, x, TRACK_BIT, sm, false);
+          if (ev > 0) {
+            const int32_t old = atomicExch(d.hm + x, 0);
+            if (old != 0 && old < n) gap_move(d, sm, 1, old, 0);
+          } else if (ev < 0 && ldv(d.hm + x) < n) activate(d, make_track(d, 1), wl0, x, TRACK_BIT, sm, false);
         }
       }
       {
@@ -1940,15 +2116,27 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(const __grid_con
     // ---- P = {h+ = |V| and h- = |V|} (Alg.8 l.29-33), vertices with slots only
     if (blockIdx.x == 0 && threadIdx.x < NB) {
       ctl->qc[threadIdx.x] = 0;
-      if (threadIdx.x < 2) { ctl->fs[threadIdx.x] = 0; ctl->mu[threadIdx.x] = 0; }
+      if (threadIdx.x < 2) { ctl->fs[threadIdx.x] = 0; ctl->mu[threadIdx.x] = 0; ctl->gtop[threadIdx.x] = 0; }
     }
+    if (blockIdx.x == 0 && d.local_gap)            // stage 2 rebuilds the level counts of P
+      for (int i = threadIdx.x; i < 2 * GAPW; i += NTHREADS) d.cnt[i] = 0;
+    long long pdef = 0, pexc = 0;                  // deficits / excess vertices in P
     for (int32_t v = gt; v < n; v += nt) {         // block-staged appends (one global atomic per CTA)
       if (d.row[v + 1] > d.row[v] && ldv(d.hp + v) >= n && ldv(d.hm + v) >= n) {
         d.part[v] = PART_P;
+        const long long ev = ldv(d.e + v);
+        pdef += ev < 0;
+        pexc += ev > 0;
         const int32_t pos = atomicAdd(&sm.acnt, 1);
         if (pos < ACAP) act_buf(sm)[pos] = v;
         else d.plist[atomicAdd(&ctl->pcnt, 1)] = v;
       }
+    }
+    pdef = bg.sum(pdef);
+    pexc = bg.sum(pexc);
+    if (threadIdx.x == 0) {
+      if (pdef) atomicAdd(&ctl->pdef, (int32_t)pdef);
+      if (pexc) atomicAdd(&ctl->pexc, (int32_t)pexc);
     }
     __syncthreads();
     {
@@ -1965,11 +2153,16 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(const __grid_con
     }
     gsync(d, grid, sm);
     const int32_t pc = cta_ld(sm, &ctl->pcnt);
+    cta_snap(sm, 2, [&](int k) { return (long long)ldv(k ? &ctl->pexc : &ctl->pdef); });
+    const bool has_def = sm.cv[0] > 0, has_exc = sm.cv[1] > 0;
     if (threadIdx.x == 0 && blockIdx.x == 0) sstat_add(sm, ST_S2_V, (unsigned long long)pc);
-    // ---- stage 2: Dynamic Push-Relabel restricted to P (Alg.8 l.34)
+    // ---- stage 2: Dynamic Push-Relabel restricted to P (Alg.8 l.34).  Its active
+    //      vertices are P's excess vertices and its roots P's deficits: with either set
+    //      empty its first global relabel would end the loop at once, so it is skipped.
     clk.lap(d, sm, ST_T_EPI);
-    if (pc > 0) {
-      device_loop(d, grid, sm, clk, RK_STAGE2, true, true);
+    if (pc > 0 && has_exc) {
+      if (has_def) device_loop(d, grid, sm, clk, RK_STAGE2, true, true);
+      else if (blockIdx.x == 0 && threadIdx.x == 0) sstat_add(sm, ST_S2_SKIP, 1);
       // ---- S_min (R19) = stage 1's final forward reach from {s} u Exc_S (h- < |V|)
       //      united with the forward reach, inside P, of the excess left in P: no
       //      residual edge enters P from S\P or leaves P towards T\P
@@ -1979,28 +2172,49 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(const __grid_con
       }
       gsync(d, grid, sm);
       device_loop(d, grid, sm, clk, RK_MINCUT_P, false, false);
+    } else if (pc > 0 && blockIdx.x == 0 && threadIdx.x == 0) {
+      sstat_add(sm, ST_S2_SKIP, 2);              // no excess in P: no stage-2 work and no P-reach
     }
     // ---- relabel partitions (Alg.8 l.35-49) and F (= sum over T' of e, R8)
     for (int32_t x = gt; x < pc; x += nt) {     // (+ the region encoding of the next warm start:
       const int32_t v = d.plist[x];              //  h+ = |V|+1 on S', h- = |V|+1 on T')
       const bool tside = ldv(d.hp + v) < n;
       d.part[v] = tside ? PART_T : PART_S;
-      if (tside) d.hm[v] = n + 1; else d.hp[v] = n + 1;
+      if (tside) d.hm[v] = n + 1;
+      else { d.hp[v] = n + 1; if (ldv(d.hm + v) > n) d.hm[v] = n; }   // (n: in S', unreached)
     }
     long long f = 0;
+    int32_t *hist = sm.cand;                     // final labels' histogram (warm start of the next call)
+    const bool want_hist = d.local_gap && d.cnt_next;
+    if (want_hist) {
+      for (int i = threadIdx.x; i < 2 * GAPW; i += NTHREADS) hist[i] = 0;
+      __syncthreads();
+    }
     for (int32_t v = gt; v < n; v += nt) {
       const long long ev = ldv(d.e + v);
       f += v == d.t ? ev : (v != d.s && ev < 0 ? ev : 0);
-      d.mask[v] = ldv(d.hm + v) < n ? 1 : 0;     // S_min, cached for dmf_min_cut_source_side
+      const int32_t hmv = ldv(d.hm + v);
+      d.mask[v] = hmv < n ? 1 : 0;               // S_min, cached for dmf_min_cut_source_side
+      if (want_hist) {
+        const int32_t hpv = ldv(d.hp + v);
+        if (hpv < n && hpv < GAPW) atomicAdd(hist + hpv, 1);
+        if (hmv < n && hmv < GAPW) atomicAdd(hist + GAPW + hmv, 1);
+      }
     }
     f = bg.sum(f);
     if (threadIdx.x == 0 && f) atomicAdd(reinterpret_cast<unsigned long long *>(&ctl->flow), (unsigned long long)f);
+    if (want_hist) {
+      __syncthreads();
+      for (int i = threadIdx.x; i < 2 * GAPW; i += NTHREADS)
+        if (hist[i]) atomicAdd(d.cnt_next + i, hist[i]);
+    }
   } else if (mode == MODE_FLOW) {
     // Stage (ii): turn the converged pseudoflow into a
     // true maximum flow.  Every vertex with excess reaches s in the residual graph
     // (Lemma 4) and every deficient vertex is reached from t;
     // neither can reach the other side at convergence, so F is unchanged.  The same
     // engine runs twice: push track with roots {s}, then pull track with roots {t}.
+    gsync(d, grid, sm);                              // (publishes the zeroed level counts)
     device_loop(d, grid, sm, clk, RK_RETURN_S, true, false);
     if (blockIdx.x == 0 && threadIdx.x < NB) {
       ctl->qc[threadIdx.x] = 0;

@@ -45,3 +45,37 @@ def test_no_oracle_import_in_product():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 txt = open(os.path.join(dp, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt and "oracle.c" not in txt, f
+
+
+def test_ctypes_structs_match_the_c_header(tmp_path):
+    """The binding's ctypes mirrors of dmf_options / dmf_stats have the C layout
+    (size and every field offset), compiled here with gcc from include/dmf.h."""
+    import ctypes
+    import paper_2511_05895_b200 as P
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "dmf.h"', 'int main(void) {']
+    for cname, cls in (("dmf_options", P.Options), ("dmf_stats", P.Stats)):
+        lines.append(f'printf("{cname} sizeof %zu\\n", sizeof({cname}));')
+        for f, _ in cls._fields_:
+            lines.append(f'printf("{cname} {f} %zu\\n", offsetof({cname}, {f}));')
+    lines.append("return 0; }")
+    src = tmp_path / "abi.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "abi"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)])
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split("\n")
+    got = {(a, b): int(c) for a, b, c in (l.split() for l in out if l)}
+    for cname, cls in (("dmf_options", P.Options), ("dmf_stats", P.Stats)):
+        assert got[(cname, "sizeof")] == ctypes.sizeof(cls), cname
+        for f, _ in cls._fields_:
+            assert got[(cname, f)] == getattr(cls, f).offset, (cname, f)
+
+
+def test_binding_rejects_mismatched_batches_without_a_gpu():
+    """Argument marshalling errors are raised before any library call."""
+    import numpy as np
+    import paper_2511_05895_b200 as P
+    f = P.DynMaxFlow.__new__(P.DynMaxFlow)     # no handle: the checks must fire first
+    with pytest.raises(ValueError):
+        f.apply_batch(np.zeros(3, np.int32), np.zeros(2, np.int32), np.zeros(3, np.int32))
+    with pytest.raises(ValueError):
+        f.apply_batch(np.zeros((2, 2), np.int32), np.zeros(4, np.int32), np.zeros(4, np.int32))

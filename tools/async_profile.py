@@ -1,20 +1,26 @@
-"""Debug build only (-DDMF_DEBUG_BUSY): event log of the asynchronous discharge phase of a
-warm DYN_PP batch on RMAT-20 -> items in flight over time and per-item durations."""
+"""Debug build only (DMF_EXTRA_NVCC=-DDMF_DEBUG_BUSY DMF_LIB=.../libdmf_debug.so): event log
+of the asynchronous discharge phase of warm DYN_PP batches on RMAT-`scale` ->
+items in flight over time, per-item durations, ring waits (enqueue -> claim -> start)."""
 import sys, os, ctypes
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import workloads as W
 import paper_2511_05895_b200 as P
-g = W.rmat(20, 16, 1, 7)
+scale = int(sys.argv[1]) if len(sys.argv) > 1 else 20
+nb = int(sys.argv[2]) if len(sys.argv) > 2 else 6
+g = W.rmat(scale, 16, 1, 7)
 f = P.DynMaxFlow.from_graph(g)
 f.static_solve()
 cs = W.CapState(g)
-for j in range(3):
+deg = np.diff(np.concatenate([[0], np.cumsum(np.bincount(np.concatenate([g.u, g.v]), minlength=g.n))]))
+for j in range(nb):
     b = W.rmat_batch(g, cs, 0.01, 100 + j); cs.apply(b)
-    if j == 2:
-        f.set_trace(1 << 17)
+    if j == nb - 1:
+        f.set_trace(1 << 20)
     f.apply_batch(b.u, b.v, b.new_cap, algo="pp")
-print("device ms", f.stats()["device_ms"], "discharge us", f.stats()["t_discharge_us"])
+st = f.stats()
+print("device ms", st["device_ms"], "discharge us", st["t_discharge_us"], "gap", st["gap_levels"], st["gap_skips"],
+      "tail_stops", st["tail_stops"], "budget_stops", st["budget_stops"])
 cnt = ctypes.c_int32()
 f._check(f._L.dmf_get_trace(f._h, None, 0, ctypes.byref(cnt)))
 buf = np.zeros(8 * max(cnt.value, 1), np.int32)
@@ -24,28 +30,50 @@ R = R[R[:, 0] >= 200]
 t = R[:, 6].astype(np.int64)
 t0 = t.min()
 ts = (t - t0) / 1000.0
-kinds = R[:, 0]
-# pair starts / ends per warp (records of one warp are sequential)
+print("records", len(R), "span us", ts.max())
+# items: start (200 vertex / 204 chunk) .. end (201 / 205) per warp
 items = []
 for w in np.unique(R[:, 2]):
     m = R[:, 2] == w
     rw, tw = R[m], ts[m]
     o = np.argsort(tw, kind="stable"); rw, tw = rw[o], tw[o]
-    st = None
+    st_ = None
     for r, tt in zip(rw, tw):
-        if r[0] in (200, 204): st = (tt, r)
-        elif r[0] in (201, 205) and st is not None:
-            items.append((st[0], tt, int(st[1][1]), int(st[1][0])))
-            st = None
-items = np.array([(a, b, v, k) for a, b, v, k in items])
-print("items", len(items), "span us", ts.max())
+        if r[0] in (200, 204): st_ = (tt, r)
+        elif r[0] in (201, 205) and st_ is not None:
+            items.append((st_[0], tt, int(st_[1][1]), int(st_[1][0]), int(r[5]) if r[0] == 201 else int(r[4])))
+            st_ = None
+items = np.array(items, dtype=np.float64)
+print("items", len(items))
 dur = items[:, 1] - items[:, 0]
 for k, name in ((200, "vertex"), (204, "chunk")):
-    d = dur[items[:, 3] == k]
-    if len(d): print(f"{name}: n={len(d)} dur p50={np.median(d):.1f} p90={np.percentile(d, 90):.1f} max={d.max():.1f} us")
+    sel = items[:, 3] == k
+    d = dur[sel]
+    if len(d):
+        dg = deg[items[sel, 2].astype(int)]
+        print(f"{name}: n={len(d)} dur p10={np.percentile(d,10):.1f} p50={np.median(d):.1f} p90={np.percentile(d, 90):.1f} max={d.max():.1f} us"
+              f"  deg p50={np.median(dg):.0f} p90={np.percentile(dg,90):.0f}")
+        for lo, hi in ((0, 2), (2, 8), (8, 17), (17, 128), (128, 513), (513, 1 << 30)):
+            ss = (dg >= lo) & (dg < hi)
+            if ss.sum():
+                print(f"   deg [{lo},{hi}): n={ss.sum()} dur p50={np.median(d[ss]):.1f} p90={np.percentile(d[ss],90):.1f}")
+# ring waits: enqueue (202, vertex a) -> claim (203, vertex a) -> next start of that vertex
+enq = R[R[:, 0] == 202]; cl = R[R[:, 0] == 203]
+te = {}
+for r, tt in zip(enq, ts[R[:, 0] == 202]):
+    te.setdefault(int(r[1]), []).append(tt)
+waits = []
+for r, tt in zip(cl, ts[R[:, 0] == 203]):
+    lst = te.get(int(r[1]))
+    if lst:
+        prev = [x for x in lst if x <= tt]
+        if prev: waits.append(tt - prev[-1])
+if waits:
+    w = np.array(waits)
+    print(f"enqueue->claim wait: n={len(w)} p50={np.median(w):.2f} p90={np.percentile(w,90):.2f} max={w.max():.1f} us")
 edges = np.arange(0, ts.max() + 10, 10)
 for lo in edges:
     hi = lo + 10
     fl = ((items[:, 0] < hi) & (items[:, 1] > lo)).sum()
-    st = ((items[:, 0] >= lo) & (items[:, 0] < hi)).sum()
-    print(f"  t={lo:6.0f}-{hi:<6.0f} in-flight {fl:5d} started {st:5d}")
+    stt = ((items[:, 0] >= lo) & (items[:, 0] < hi)).sum()
+    print(f"  t={lo:6.0f}-{hi:<6.0f} in-flight {fl:5d} started {stt:5d}")

@@ -275,6 +275,31 @@ def _weighted_sample(r: np.random.Generator, w: np.ndarray, k: int) -> np.ndarra
     return idx[r.permutation(k)]
 
 
+def _weighted_sample_two_class(r: np.random.Generator, m: int, heavy: np.ndarray, bias: float, k: int) -> np.ndarray:
+    """The same distribution as _weighted_sample (Efraimidis-Spirakis top-k of
+    log(U)/w) when every weight is 1 except weight `bias` on the sorted indices
+    `heavy`, in O(k + |heavy|) instead of O(m): the heavy keys are drawn as they are;
+    of the weight-1 class only its k largest keys can reach the overall top k, and the
+    k largest of M iid log(U) are -(Z_1/M + Z_2/(M-1) + ...) (Exp(1) spacings, Renyi)
+    sitting on a uniformly random k-subset of the class (ranks independent of values)."""
+    k = min(k, m)
+    nh = heavy.shape[0]
+    ma = m - nh
+    kh = np.log(r.random(nh)) / bias
+    ka_n = min(k, ma)
+    z = r.exponential(1.0, size=ka_n) / (ma - np.arange(ka_n, dtype=np.float64))
+    ka = -np.cumsum(z)
+    pos = r.choice(ma, size=ka_n, replace=False) if ka_n else np.zeros(0, np.int64)
+    # pos-th element of the light class = pos + number of heavy indices before it
+    shift = heavy - np.arange(nh)
+    a_idx = pos + np.searchsorted(shift, pos, side="right")
+    keys = np.concatenate([kh, ka])
+    cand = np.concatenate([heavy.astype(np.int64), a_idx.astype(np.int64)])
+    top = np.argpartition(-keys, k - 1)[:k] if k < keys.shape[0] else np.arange(keys.shape[0])
+    idx = np.sort(cand[top])
+    return idx[r.permutation(idx.shape[0])]
+
+
 def rmat_batch(g: Graph, st: CapState, frac: float, seed: int, kind: str = "mix",
                bias: float = 10.0, capmax: int = 1000) -> Batch:
     """Batch of round(frac*m) distinct existing input edges, weight `bias` on
@@ -282,9 +307,11 @@ def rmat_batch(g: Graph, st: CapState, frac: float, seed: int, kind: str = "mix"
     (R20); mix = ceil(k/2) inc + floor(k/2) dec."""
     r = _rng(seed)
     k = max(1, int(round(frac * g.m)))
-    w = np.ones(g.m, np.float64)
-    w[(g.u == g.s) | (g.v == g.t)] = bias
-    idx = _weighted_sample(r, w, k)
+    heavy = g.meta.get("_heavy")
+    if heavy is None:
+        heavy = np.nonzero((g.u == g.s) | (g.v == g.t))[0]
+        g.meta["_heavy"] = heavy
+    idx = _weighted_sample_two_class(r, g.m, heavy, bias, k)
     u = g.u[idx]
     v = g.v[idx]
     old = st.lookup(u, v)
