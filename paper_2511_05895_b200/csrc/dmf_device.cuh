@@ -81,6 +81,7 @@ struct Ctl {
   int32_t atail;                // async: item completions while <= TAIL_PEND items were pending
   int32_t gtop[2];              // local gap per track: 0 = none, else GAPW - (lowest emptied level)
   int32_t tact[3];              // topology round r: some vertex became (or stayed) active [r % 3]
+  int32_t tcq[3 * NB];          // topology round r: counts of the sweep's chunk list [r % 3][bin]
   int32_t check;                // invariant check: first violated check (0 = none) and a witness
   int32_t check_at;
   int32_t pdef, pexc;           // DYN_PP: deficit / excess vertices in P (stage 2 / P-reach skip)

@@ -1646,7 +1646,7 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
       if (threadIdx.x == 0) { ctl->aw = 0; ctl->ahead = 0; ctl->astop = 0; ctl->awork = 0; ctl->atail = 0; }
       rlc[threadIdx.x] = 0;
       qc[NB + threadIdx.x] = 0;
-      if (threadIdx.x < 3) ctl->work[threadIdx.x] = 0;
+      if (threadIdx.x < 3) { ctl->work[threadIdx.x] = 0; ctl->tact[threadIdx.x] = 0; }
       if (threadIdx.x < 2) { ctl->fs[2 + threadIdx.x] = 0; ctl->bulc[threadIdx.x] = 0; }
     }
     const int32_t N = on_plist ? cta_ld(sm, &ctl->pcnt) : n;
@@ -1803,21 +1803,22 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
     __syncthreads();
     if (topo) {
       for (int r = 0;; ++r) {
-        // rings of 3 as in the rounds below, shifted by one: slot 0 of wlc holds the BFS
-        // worklist counts (unused here) when round 0 starts
-        const int cur = (r + 1) % 3, nx = (r + 2) % 3, nn = r % 3;
+        // rings of 3 (round r uses slot r % 3, zeroes slot (r+1) % 3, last read in
+        // round r-2): activity flag, work and the chunk-list count of the sweep.  (Not
+        // wlc: other CTAs may still be reading the BFS worklist counts in slot 0.)
+        const int cur = r % 3, nx = (r + 1) % 3;
         if (threadIdx.x == 0) sm.tslot = cur;
         if (blockIdx.x == 0 && threadIdx.x < NB) {
-          wlc[NB * nn + threadIdx.x] = 0;         // (same ring discipline as the rounds below)
+          ctl->tcq[NB * nx + threadIdx.x] = 0;
           if (threadIdx.x == 0) { ctl->tact[nx] = 0; ctl->work[nx] = 0; }
         }
         __syncthreads();
-        const BL tch{L.wl1, wlc + NB * cur, n, L.cw1};   // chunks of the big active vertices of this sweep
+        const BL tch{L.wl1, ctl->tcq + NB * cur, n, L.cw1};   // chunks of the big active vertices of this sweep
         topology_sweep(d, sm, on_plist ? d.plist : nullptr, ndom, use0, use1, rl, tch);
         dis_flush(d, sm, tch, rl);
         gsync(d, grid, sm);
         {
-          const int32_t nc = cta_ld(sm, wlc + NB * cur + 3);
+          const int32_t nc = cta_ld(sm, ctl->tcq + NB * cur + 3);
           const int32_t gw = blockIdx.x * WPB + (threadIdx.x >> 5), nw = gridDim.x * WPB;
           for (int32_t x = gw; x < nc; x += nw) discharge_chunk(d, sm, tch.cq[x], rl, tch);
           dis_flush(d, sm, tch, rl);
@@ -1899,7 +1900,7 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
     }
     // ---------------- RIE over the vertices relabelled in this iteration
     if (blockIdx.x == 0 && threadIdx.x < NB) {
-      for (int q = 0; q < 3; q++) wlc[NB * q + threadIdx.x] = 0;
+      for (int q = 0; q < 3; q++) { wlc[NB * q + threadIdx.x] = 0; ctl->tcq[NB * q + threadIdx.x] = 0; }
       if (threadIdx.x < 3) for (int q = 0; q < 3; q++) ctl->claim[3 * q + threadIdx.x] = 0;
       qc[threadIdx.x] = 0;                        // for the next RESET
       if (threadIdx.x < 2) { ctl->fs[threadIdx.x] = 0; ctl->mu[threadIdx.x] = 0; ctl->gtop[threadIdx.x] = 0; }

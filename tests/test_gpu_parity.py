@@ -360,80 +360,98 @@ def test_to_flow_rmat(dmf, scale, algo):
 
 # ------------------------------------------------------------------ full-size configs
 # BASELINE.json configs 2-5 at full size, in the launch configuration bench.py times
-# (default grid, KERNELCYCLES = floor(m/n)).  F and S_min are compared bit-exactly
-# with the oracle (two-phase FIFO push-relabel) after the static solve and after
-# every batch; the exported state passes the checker where noted.
+# (default grid, KERNELCYCLES = floor(m/n), default knobs).  F and S_min are compared
+# bit-exactly with the oracle (two-phase FIFO push-relabel, a full recompute per
+# batch on a pool of worker processes: oracle/pool.py) after the static solve and
+# after EVERY batch.
 
-def _full_run(dmf, g, batches, algos, check_states=(0,)):
-    f = dmf.DynMaxFlow.from_graph(g)
+def _replay(dmf, spec, algos, check_at=(), knobs=None):
+    """Static solve + the batches of `spec` on one handle; returns per-batch (F, S_min)
+    (index -1 = after the static solve) and the handle."""
+    g, batches = W.sequence(spec)
+    f = dmf.DynMaxFlow.from_graph(g, **(knobs or {}))
     f.static_solve()
-    st = W.CapState(g)
-    _verify_full(f, g, "static", check=0 in check_states)
-    for j, (b, algo) in enumerate(zip(batches(st), algos)):
-        st.apply(b)
-        f.apply_batch(b.u, b.v, b.new_cap, algo=algo)
-        _verify_full(f, st.graph(), f"b{j} {algo}", check=(j + 1) in check_states)
-    return f
+    got = {-1: (f.flow_value(), f.min_cut_source_side().copy())}
+    for j, b in enumerate(batches):
+        f.apply_batch(b.u, b.v, b.new_cap, algo=algos[j % len(algos)])
+        got[j] = (f.flow_value(), f.min_cut_source_side().copy())
+        if j in check_at:
+            st = W.CapState(g)
+            for bb in batches[:j + 1]:
+                st.apply(bb)
+            gg = st.graph()
+            stt = f.export_state()
+            rc, msg, _ = O.check_state(gg.n, gg.s, gg.t, stt["row_ptr"], stt["dst"], stt["rev"], stt["cap"],
+                                       stt["res"], stt["e"], got[j][0], got[j][1])
+            assert rc == 0, f"b{j}: checker {rc}: {msg}"
+    return got, f
 
 
-def _verify_full(f, g, tag, check):
-    r = O.maxflow(g, "fifo_pr")
-    F = f.flow_value()
-    assert F == r["F"], f"{tag}: F gpu={F} oracle={r['F']}"
-    smin = f.min_cut_source_side()
-    assert np.array_equal(smin, r["smin"]), f"{tag}: S_min differs ({int((smin != r['smin']).sum())} vertices)"
-    if check:
-        stt = f.export_state()
-        rc, msg, _ = O.check_state(g.n, g.s, g.t, stt["row_ptr"], stt["dst"], stt["rev"], stt["cap"], stt["res"],
-                                   stt["e"], F, smin)
-        assert rc == 0, f"{tag}: checker {rc}: {msg}"
-
-
-def _rmat_batches(g, fracs, seed0):
-    def gen(st):
-        for j, fr in enumerate(fracs):
-            b = W.rmat_batch(g, st, fr, seed0 + j)
-            yield b
-    return gen
+def _compare(spec, got, tag):
+    from oracle.pool import recompute
+    res = recompute(spec, sorted(got))
+    assert len(res) == len(got), f"{tag}: oracle finished {len(res)} of {len(got)} recomputes"
+    for r in res:
+        F, smin = got[r["j"]]
+        assert F == r["F"], f"{tag} b{r['j']}: F gpu={F} oracle={r['F']}"
+        assert np.array_equal(smin, r["smin"]), \
+            f"{tag} b{r['j']}: S_min differs ({int((smin != r['smin']).sum())} vertices)"
 
 
 @pytest.mark.full
-def test_config2_rmat20_full(dmf):
-    """Config 2: RMAT-20 (1M / 16.1M), 1% / 0.1% / 10% mixed batches, PP and PR."""
-    g = W.config_graph("rmat20")
-    _full_run(dmf, g, _rmat_batches(g, [0.01, 0.001, 0.1, 0.01], 100), ["pp", "pr", "pp", "pr"], check_states=(0, 1))
+@pytest.mark.parametrize("workload", ["rmat22", "rmat20"])
+def test_bench_sequence_full(dmf, workload):
+    """EXACTLY the batches bench.py times (its workload spec, warm-up + timed steps), in
+    its launch configuration, DYN_PP, checked after every batch."""
+    import bench
+    spec = bench.workload_spec(workload, bench.DEFAULT_WARMUP, bench.DEFAULT_STEPS)
+    got, f = _replay(dmf, spec, ["pp"], check_at=(0,))
+    f.close()
+    _compare(spec, got, workload)
+
+
+@pytest.mark.full
+def test_config2_rmat20_mixed_fractions_full(dmf):
+    """Config 2: RMAT-20 (1M / 16.1M), 1% / 0.1% / 10% mixed batches, PP and PR interleaved."""
+    specs = [dict(kind="rmat", scale=20, frac=fr, nb=3, seed_base=100 + 10 * i) for i, fr in enumerate([0.001, 0.1])]
+    for spec in specs:
+        got, f = _replay(dmf, spec, ["pr", "pp"], check_at=(1,))
+        f.close()
+        _compare(spec, got, f"rmat20 frac {spec['frac']}")
 
 
 @pytest.mark.full
 def test_config3_grid2048_full(dmf):
-    """Config 3: 2048x2048 segmentation grid, terminal-capacity batches (0.1% / 1% of pixels)."""
-    g = W.config_graph("grid2048")
-
-    def gen(st):
-        for j, fr in enumerate([0.01, 0.001, 0.01]):
-            yield W.grid_batch(g, fr, 300 + j)
-    _full_run(dmf, g, gen, ["pr", "pp", "pp"], check_states=(1,))
+    """Config 3: 2048x2048 segmentation grid, 10 terminal-capacity batches (1% of pixels),
+    PR and PP interleaved."""
+    spec = dict(kind="grid", W=2048, seed=3, frac=0.01, nb=10, seed_base=300)
+    got, f = _replay(dmf, spec, ["pr", "pp"], check_at=(3,))
+    f.close()
+    _compare(spec, got, "grid2048")
 
 
 @pytest.mark.full
-def test_config4_bipartite_full(dmf):
-    """Config 4: unit bipartite 4M+4M / 72.7M merged edges; F = Hopcroft-Karp matching;
-    one 1% insert/delete batch with PP."""
-    g = W.config_graph("bip4m")
+@pytest.mark.parametrize("algo", ["pp", "pr"])
+def test_config4_bipartite_full(dmf, algo):
+    """Config 4: unit bipartite 4M+4M / 72.7M merged edges; static F = Hopcroft-Karp
+    matching; 3 cumulative 1% insert/delete batches under PR and under PP."""
+    spec = dict(kind="bip", frac=0.01, nb=3, seed_base=400)
+    g, _ = W.sequence(dict(spec, nb=0))
     L = g.meta["L"]
     a, b_ = g.meta["lr_begin"], g.meta["lr_end"]
     lr = g.cap[a:b_] > 0
-    f = dmf.DynMaxFlow.from_graph(g)
-    assert f.static_solve() == O.hopcroft_karp(L, L, g.u[a:b_][lr], g.v[a:b_][lr] - L)
-    st = W.CapState(g)
-    b = W.bipartite_batch(g, st, 0.01, 400)
-    st.apply(b)
-    f.apply_batch(b.u, b.v, b.new_cap, algo="pp")
-    _verify_full(f, st.graph(), "bip b0 pp", check=False)
+    got, f = _replay(dmf, spec, [algo])
+    f.close()
+    assert got[-1][0] == O.hopcroft_karp(L, L, g.u[a:b_][lr], g.v[a:b_][lr] - L)
+    del got[-1]
+    _compare(spec, got, f"bip {algo}")
 
 
 @pytest.mark.full
-def test_config5_rmat22_snapshot_full(dmf):
-    """Config 5 (one snapshot per GPU): RMAT-22 (4.2M / 65.2M), 1% PP batches."""
-    g = W.config_graph("rmat22_1")
-    _full_run(dmf, g, _rmat_batches(g, [0.01, 0.01], 100), ["pp", "pp"], check_states=())
+def test_config5_rmat22_snapshots_full(dmf):
+    """Config 5: two more RMAT-22 snapshots (graph seeds 2 and 3), 3 PP batches each."""
+    for seed in (2, 3):
+        spec = dict(kind="rmat", scale=22, seed_graph=seed, frac=0.01, nb=3, seed_base=100)
+        got, f = _replay(dmf, spec, ["pp"])
+        f.close()
+        _compare(spec, got, f"rmat22 seed {seed}")

@@ -49,3 +49,24 @@ def test_reduce_gloo_world2():
     for r in range(2):
         u, ms, eu, ems = out[r]
         assert u == 350.0 and ms == 5.0 and eu == 175.0 and ems == 10.0
+
+
+def test_bench_launcher_spawns_ranks_gloo():
+    """`bench.py --gpus 2` without a launcher re-executes itself under
+    torch.distributed.run with 2 ranks; --stub runs the rank bookkeeping on CPU (gloo):
+    4 snapshots -> rank 0 takes {0, 2}, rank 1 {1, 3}; whole-job units = SUM, time = MAX."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ)
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"):
+        env.pop(k, None)
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--snapshots", "4", "--stub"],
+                         capture_output=True, text=True, env=env, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["snapshots_rank0"] == [0, 2]
+    assert line["units_all"] == 1000 + 2000 + 3000 + 4000          # every snapshot counted once
+    assert line["ms_max"] == max(10 + 30, 20 + 40)                   # slowest rank
+    assert abs(line["value"] - 10000 / 0.060) < 1e-6

@@ -459,3 +459,34 @@ def config_graph(name: str) -> Graph:
     if name == "bip4m":
         return bipartite()
     raise KeyError(name)
+
+
+def sequence(spec: dict):
+    """(graph, list of batches) of a named cumulative batch sequence, deterministic in
+    `spec` (picklable, so that oracle workers can rebuild it):
+      {"kind": "rmat", "scale": 20, "seed_graph": 1, "seed_caps": 7, "frac": 0.01,
+       "nb": 25, "seed_base": 100}
+      {"kind": "grid", "W": 2048, "seed": 3, "frac": 0.01, "nb": 10, "seed_base": 300}
+      {"kind": "bip", "L": 2**22, "draws": 2**26, "seed": 4, "frac": 0.01, "nb": 3, "seed_base": 400}
+    Batch j is drawn after batches 0..j-1 were applied (cumulative capacities)."""
+    kind = spec["kind"]
+    if kind == "rmat":
+        g = rmat(spec["scale"], spec.get("edge_factor", 16), spec.get("seed_graph", 1), spec.get("seed_caps", 7))
+        gen = lambda st, j: rmat_batch(g, st, spec["frac"], spec.get("seed_base", 100) + j)  # noqa: E731
+    elif kind == "grid":
+        g = grid(spec["W"], spec.get("seed", 3))
+        gen = lambda st, j: grid_batch(g, spec["frac"], spec.get("seed_base", 300) + j)  # noqa: E731
+    elif kind == "bip":
+        g = bipartite(L=spec.get("L", 1 << 22), draws=spec.get("draws", 1 << 26), seed=spec.get("seed", 4))
+        gen = lambda st, j: bipartite_batch(g, st, spec["frac"], spec.get("seed_base", 400) + j)  # noqa: E731
+    else:
+        raise KeyError(kind)
+    st = CapState(g)
+    out = []
+    for j in range(spec["nb"]):
+        b = gen(st, j)
+        st.apply(b)
+        out.append(b)
+    if kind == "grid":        # grid_batch drifts the image in g.meta: rebuild it unperturbed
+        g = grid(spec["W"], spec.get("seed", 3))
+    return g, out
