@@ -182,6 +182,7 @@ def run_snapshot(P, torch, dev, spec, W_, K, algo, no_cut=False):
     fa.static_solve()
     out["F_static_initial"] = fa.flow_value()
     raw = [P.Stats() for _ in batches]
+    qms = []
     for j in range(W_):
         u, v, c = dbat[j]
         fa.apply_batch(u, v, c, algo=algo)
@@ -198,12 +199,14 @@ def run_snapshot(P, torch, dev, spec, W_, K, algo, no_cut=False):
         fa.raw_stats(raw[j])
         if not no_cut:
             fa.min_cut_source_side(dmask)
+            qms.append(fa.raw_stats().query_ms)
         ev[i + 1].record(stream)
     torch.cuda.synchronize()
     out["elapsed_ms"] = ev[0].elapsed_time(ev[K])
     out["step_ms"] = [ev[i].elapsed_time(ev[i + 1]) for i in range(K)]
     out["launches"] = fa.stats()["kernel_launches"] - launches0
     out["per"] = [P.DynMaxFlow.stats_to_dict(raw[j]) for j in range(W_, W_ + K)]
+    out["query_ms"] = qms
     out["F_final"] = fa.flow_value()
     out["k_timed"] = int(sum(batches[j].k for j in range(W_, W_ + K)))
     fa.close()
@@ -235,7 +238,7 @@ def run_snapshot(P, torch, dev, spec, W_, K, algo, no_cut=False):
     # ---- C: static re-solve of every timed capacity snapshot (the paper's baseline)
     fc = P.DynMaxFlow.from_graph(g, algo=algo)
     fc.static_solve()
-    st_alg1, st_pp = [], []
+    st_alg1, st_pp, st_cut = [], [], []
     for j in range(W_ + K):
         u, v, c = dbat[j]
         fc.apply_batch(u, v, c, algo="pp")
@@ -248,10 +251,14 @@ def run_snapshot(P, torch, dev, spec, W_, K, algo, no_cut=False):
         fc.static_solve_pp()
         st_pp.append(fc.stats()["device_ms"])
         assert fc.flow_value() == Fd
+        if not no_cut:
+            fc.min_cut_source_side(dmask)              # S_min of the static solution (MINCUT launch)
+            st_cut.append(fc.raw_stats().query_ms)
     out["static_stats"] = fc.stats()
     fc.close()
     out["static_alg1_ms"] = st_alg1
     out["static_pp_ms"] = st_pp
+    out["static_cut_ms"] = st_cut
     return out
 
 
@@ -266,7 +273,16 @@ def summarize(snaps, K, peak):
     km = float(np.mean(batch_ms))
     ab = float(np.mean(alg))
     med = lambda key: float(np.median([p[key] for p in per]))  # noqa: E731
+    qms = [x for s in snaps for x in s["query_ms"]]
+    scut = [x for s in snaps for x in s["static_cut_ms"]]
+    with_cut = None
+    if qms and scut:
+        with_cut = (float(np.median(static_ms)) + float(np.median(scut))) / \
+                   (float(np.median(batch_ms)) + float(np.median(qms)))
     return {
+        "cut_query_ms": {"p50": pctl(qms, 50), "p90": pctl(qms, 90),
+                         "static_p50": pctl(scut, 50)} if qms else None,
+        "speedup_vs_static_with_cut": with_cut,
         "batch_ms": {"p50": pctl(batch_ms, 50), "p90": pctl(batch_ms, 90), "mean": km},
         "static_ms": {"p50": pctl(static_ms, 50), "p90": pctl(static_ms, 90),
                       "alg1_p50": pctl([x for s in snaps for x in s["static_alg1_ms"]], 50),
@@ -459,7 +475,8 @@ def main():
                      "value": s20["k_timed"] / (s20["elapsed_ms"] * 1e-3),
                      "e2e_value": s20["k_timed"] / (s20["e2e_ms"] * 1e-3),
                      "ms_per_step": s20["elapsed_ms"] / K,
-                     **{k: sm20[k] for k in ("batch_ms", "static_ms", "speedup_vs_static", "roofline",
+                     **{k: sm20[k] for k in ("batch_ms", "static_ms", "speedup_vs_static",
+                                               "speedup_vs_static_with_cut", "cut_query_ms", "roofline",
                                                "phase_us_median")}}
         traffic = None
         tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -494,6 +511,8 @@ def main():
             "batch_apply_ms": summ["batch_ms"],
             "static_solve_ms": summ["static_ms"],
             "speedup_vs_static": summ["speedup_vs_static"],
+            "speedup_vs_static_with_cut": summ["speedup_vs_static_with_cut"],
+            "cut_query_ms": summ["cut_query_ms"],
             "speedup_vs_static_per_batch": summ["speedup_vs_static_per_batch"],
             "step_ms": summ["step_ms"], "e2e_step_ms": summ["e2e_step_ms"],
             "edges_per_s": summ["edges_per_s"], "static_edges_per_s": summ["static_edges_per_s"],

@@ -107,7 +107,13 @@ typedef struct {
                                invariants (0 <= res <= cap + cap_rev, res[i] + res[rev[i]] = cap[i] +
                                cap[rev[i]], mirror consistency, sum of e = 0) and the call fails with
                                DMF_ECHECK if one is violated [DMF_CHECK_LEVEL] */
-    int32_t reserved[8];    /* must be zero */
+    int32_t certify;        /* DYN_PP after DYN_PP: after the warm discharge iteration, test convergence
+                               with the universal certificate (reading R9: a fresh backward BFS from
+                               {t} u {deficient vertices} reaches no excess vertex and s reaches none of
+                               its labels); when it holds the call ends there (partition = that BFS's
+                               reach, R15) and S_min is computed by dmf_min_cut_source_side on demand.
+                               0 => on, < 0 => off (always the full Alg.8 stage 1 / P / stage 2) [DMF_CERTIFY] */
+    int32_t reserved[7];    /* must be zero */
 } dmf_options;
 
 typedef struct {
@@ -144,6 +150,9 @@ typedef struct {
     int64_t topology_rounds;   /* discharge rounds run topology-driven */
     int64_t tail_stops;        /* ASYNC phases ended by the progress stop (tail_items) */
     int64_t stage2_skipped;    /* DYN_PP: stage 2 / the P-reach skipped (P holds no deficit / no excess) */
+    int64_t certified;         /* DYN_PP: 1 if the warm iteration was certified converged (options.certify) */
+    float   query_ms;          /* device time of the last dmf_min_cut_source_side / dmf_max_cut_source_side
+                                  launch (0 when S_min was already cached by the last DYN_PP call) */
 } dmf_stats;
 
 /* Fill *opt with defaults (all zero / NULL; algo = DMF_DYN_PP). */

@@ -38,10 +38,12 @@ class Options(ctypes.Structure):
                 ("free", _FREE_T), ("alloc_ctx", ctypes.c_void_p),
                 ("schedule", ctypes.c_int32), ("async_warps", ctypes.c_int32), ("budget_mul", ctypes.c_int32),
                 ("tail_items", ctypes.c_int32), ("local_gap", ctypes.c_int32), ("warm", ctypes.c_int32),
-                ("topo_div", ctypes.c_int32), ("check_level", ctypes.c_int32), ("reserved", ctypes.c_int32 * 8)]
+                ("topo_div", ctypes.c_int32), ("check_level", ctypes.c_int32), ("certify", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 7)]
 
 
-KNOBS = ("schedule", "async_warps", "budget_mul", "tail_items", "local_gap", "warm", "topo_div", "check_level")
+KNOBS = ("schedule", "async_warps", "budget_mul", "tail_items", "local_gap", "warm", "topo_div", "check_level",
+         "certify")
 
 
 class Stats(ctypes.Structure):
@@ -58,7 +60,8 @@ class Stats(ctypes.Structure):
                 ("device_ms", ctypes.c_float), ("t_prologue_us", ctypes.c_float), ("t_reset_us", ctypes.c_float),
                 ("t_bfs_us", ctypes.c_float), ("t_discharge_us", ctypes.c_float), ("t_rie_us", ctypes.c_float),
                 ("t_epilogue_us", ctypes.c_float), ("gap_levels", ctypes.c_int64), ("gap_skips", ctypes.c_int64),
-                ("topology_rounds", ctypes.c_int64), ("tail_stops", ctypes.c_int64), ("stage2_skipped", ctypes.c_int64)]
+                ("topology_rounds", ctypes.c_int64), ("tail_stops", ctypes.c_int64), ("stage2_skipped", ctypes.c_int64),
+                ("certified", ctypes.c_int64), ("query_ms", ctypes.c_float)]
 
 
 class DMFError(RuntimeError):

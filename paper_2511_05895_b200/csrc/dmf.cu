@@ -78,6 +78,7 @@ struct dmf_graph {
   int32_t local_gap = 1;
   int32_t topo_div = 16;
   int32_t check_level = 0;
+  int32_t lazy = 1;          // DYN_PP warm start certified by the universal backward BFS
   long long budget_mul = 1;
   int32_t *cnt = nullptr, *cnt_next = nullptr;   // local-gap level counts (this call / next warm call)
   int32_t *chk = nullptr;                          // invariant check scratch (64 bytes)
@@ -285,6 +286,7 @@ static Dev make_dev(dmf_graph *g) {
   d.cnt = g->cnt; d.cnt_next = g->cnt_next;
   d.local_gap = g->local_gap; d.topo_div = g->topo_div; d.tail_items = g->tail_items;
   d.check_level = g->check_level;
+  d.lazy = g->lazy;
   d.plist = g->plist; d.stamp = g->stamp;
   d.mask = g->mask; d.ctl = g->ctl;
   d.dbg = g->ddbg;
@@ -387,6 +389,7 @@ static int run_solve(dmf_graph *g, int32_t mode, const Dev &dv) {
   st.topology_rounds = (int64_t)c.stat[ST_TOPO_ROUNDS];
   st.tail_stops = (int64_t)c.stat[ST_TAIL_STOPS];
   st.stage2_skipped = (int64_t)c.stat[ST_S2_SKIP];
+  st.certified = c.lazy_ok;
   st.batch_entries = dv.k;
   st.device_ms = ms;
   if (c.pad != 0) fprintf(stderr, "[dmf debug] vertex %d discharged concurrently\n", c.pad - 1);
@@ -420,8 +423,10 @@ static int run_solve(dmf_graph *g, int32_t mode, const Dev &dv) {
   }
   // MAXCUT / STATIC / PR leave no S_min; FLOW keeps it (stage (ii) moves flow only
   // inside S_max and inside T, and S_min of a maximum flow is unique)
-  g->smin_valid = mode == MODE_PP || mode == MODE_MINCUT || (mode == MODE_FLOW && smin_before);
-  g->warm = mode == MODE_PP && !g->no_warm;
+  g->smin_valid = (mode == MODE_PP && !c.lazy_ok) || mode == MODE_MINCUT || (mode == MODE_FLOW && smin_before);
+  // DYN_PP leaves its final labels for the next DYN_PP; MINCUT refreshes h- (exact
+  // forward distances) and keeps a warm start warm; every other launch ends it
+  g->warm = (mode == MODE_PP && !g->no_warm) || (mode == MODE_MINCUT && warm_before);
   if (g->warm && g->local_gap) std::swap(g->cnt, g->cnt_next);   // the final labels' histogram
   if (g->check_level > 0 && mode != MODE_MINCUT && mode != MODE_MAXCUT) {
     const int rc = check_state(g);
@@ -598,11 +603,12 @@ int dmf_create(int32_t n, const int64_t *row_ptr, const int32_t *col, const int3
     if (const char *nw = getenv("DMF_NO_WARM")) g->no_warm = atoi(nw) != 0;
     const int32_t td = knob(o.topo_div, "DMF_TOPO_DIV");
     g->topo_div = sched == DMF_SCHED_TOPOLOGY ? 0x3fffffff : (td == 0 ? 16 : (td < 0 ? 0 : td));
+    g->lazy = knob(o.certify, "DMF_CERTIFY") < 0 ? 0 : 1;
     g->check_level = knob(o.check_level, "DMF_CHECK_LEVEL");
     if (const char *ba = getenv("DMF_BU_ALPHA")) g->bu_alpha = atoi(ba) > 0 ? atoi(ba) : g->bu_alpha;
     if (const char *dd = getenv("DMF_DENSE_DIV")) g->dense_div = atoi(dd) > 0 ? atoi(dd) : g->dense_div;
     if (const char *sl = getenv("DMF_ASYNC_SLEEP_NS")) g->async_sleep_ns = atoi(sl) > 0 ? atoi(sl) : 1024;
-    for (int i = 0; i < 8; i++)
+    for (int i = 0; i < 7; i++)
       if (o.reserved[i]) { fail(DMF_EINVAL, "dmf_options.reserved must be zero"); return bail(DMF_EINVAL); }
   }
   g->chk = (int32_t *)g->alloc(64);
@@ -732,8 +738,11 @@ static int cut_query(dmf_graph *g, uint8_t *mask, int32_t mode) {
     dmf_stats keep = g->stats;
     Dev d = make_dev(g);
     int rc = run_solve(g, mode, d);
+    keep.query_ms = g->stats.device_ms;
     g->stats = keep;
     if (rc) return rc;
+  } else {
+    g->stats.query_ms = 0.f;
   }
   CK(cudaMemcpyAsync(mask, g->mask, (size_t)g->n, cudaMemcpyDefault, g->stream));
   CK(cudaStreamSynchronize(g->stream));

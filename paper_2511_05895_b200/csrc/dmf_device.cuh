@@ -85,6 +85,8 @@ struct Ctl {
   int32_t check;                // invariant check: first violated check (0 = none) and a witness
   int32_t check_at;
   int32_t pdef, pexc;           // DYN_PP: deficit / excess vertices in P (stage 2 / P-reach skip)
+  int32_t sreach;               // DYN_PP certificate: s reaches a vertex labelled by the backward BFS
+  int32_t lazy_ok;              // DYN_PP: converged by the certificate (no S_min mask computed)
 };
 
 // Everything a kernel needs, passed by value.  Slot arrays are SoA int32[S]:
@@ -132,6 +134,7 @@ struct Dev {
   int32_t topo_div;          // topology-driven phase when > n / topo_div vertices are active (0: never)
   int32_t tail_items;        // async progress stop (<= 0: off)
   int32_t check_level;
+  int32_t lazy;              // DYN_PP warm start: certify with the universal backward BFS (no pull BFS / stage 2)
   int32_t *plist;            // region P of push-pull stage 2
   int32_t *stamp;            // per-slot batch stamp (duplicate detection)
   const int32_t *bu, *bv, *bc;  // batch entries

@@ -1624,19 +1624,28 @@ __device__ __forceinline__ void topology_sweep(const Dev &d, Smem &sm, const int
 //   bulc[l&1]   appended in pass A of level l, read in pass B; [(l+1)&1] zeroed at l
 //   mu          accumulated in RESET, read at level 0; zeroed with qc[0]
 // Requires qc[0], fs[0], mu == 0 and wlc == 0 on entry.
-__device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseClock &clk, int kind,
-                            bool collect, bool stage2, bool warm = false) {
+// Returns 0 when the loop ended normally.  `lazy` (DYN_PP warm start, DESIGN.md
+// "certificate"): after the warm iteration the termination test is the universal one of
+// R9 -- a fresh backward BFS from {t} u {all deficits} over the whole graph (kind
+// RK_PUSH) that reaches no excess vertex, and s reaching none of its labelled vertices;
+// then the loop returns 1 (converged; the partition is that BFS's reach, R15).  If the
+// test fails it returns -1 with its queued flags dropped and the counters zeroed, and
+// the caller continues with the full Alg.8 stage 1.
+__device__ int device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseClock &clk, int kind0,
+                           bool collect, bool stage2, bool warm = false, bool lazy = false) {
   const size_t nb = (size_t)NB * d.n;
   const Lists L{d.q0, d.q1, d.cq0, d.cq1, d.wl, d.wl + nb, d.rl, d.cqr, d.cw0, d.cw1};
   const int32_t n = d.n;
   Ctl *ctl = d.ctl;
   int32_t *qc = ctl->qc, *wlc = ctl->wlc, *rlc = ctl->rlc;
   const int32_t nt = gridDim.x * NT;
-  const bool use0 = kind != RK_MINCUT && kind != RK_MINCUT_P && kind != RK_FILL_T;
-  const bool use1 = kind == RK_PP || kind == RK_MINCUT || kind == RK_MINCUT_P || kind == RK_FILL_T;
-  const bool on_plist = kind == RK_STAGE2 || kind == RK_MINCUT_P;
   const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
   for (int iter = 0;; ++iter) {
+   const bool certify = lazy && iter >= 1;       // the universal certificate pass
+   const int kind = certify ? (int)RK_PUSH : kind0;
+   const bool use0 = kind != RK_MINCUT && kind != RK_MINCUT_P && kind != RK_FILL_T;
+   const bool use1 = kind == RK_PP || kind == RK_MINCUT || kind == RK_MINCUT_P || kind == RK_FILL_T;
+   const bool on_plist = kind == RK_STAGE2 || kind == RK_MINCUT_P;
    // warm start (DYN_PP after DYN_PP): iteration 0 discharges the worklist seeded by
    // the batch prologue on the previous call's final labels; the fresh BFS of
    // iteration 1 still decides termination (R9), so stale labels cost work only
@@ -1777,6 +1786,35 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
     {
       int32_t w0[NB];
       cta_counts(sm, wlc, w0);
+      if (certify) {
+        // s is never labelled by the backward BFS (h+(s) = |V|, R1) and DYN_PP does not
+        // re-saturate s (R16): s must reach no labelled vertex either
+        if (total(w0) == 0) {
+          const int32_t sb = d.row[d.s], se = d.row[d.s + 1];
+          bool hit = false;
+          for (int32_t i = sb + blockIdx.x * NT + threadIdx.x; i < se; i += nt)
+            hit |= ldv(d.res + i) > 0 && ldv(d.hp + d.dst[i]) < n;
+          if (__syncthreads_or(hit) && threadIdx.x == 0) atomicExch(&ctl->sreach, 1);
+          gsync(d, grid, sm);
+          if (cta_ld(sm, &ctl->sreach) == 0) return 1;     // converged (R9)
+        }
+        // not certified: drop the queued flags of the collected worklist, clear the
+        // counters device_loop expects zero, and hand back to the full stage 1
+        for (int32_t x = blockIdx.x * NT + threadIdx.x; x < w0[0] + w0[1]; x += nt)
+          d.inq[(uint32_t)(x < w0[0] ? L.wl0[x] : L.wl0[(size_t)d.n + x - w0[0]]) & ~TRACK_BIT] = 0;
+        for (int32_t x = blockIdx.x * NT + threadIdx.x; x < w0[3]; x += nt)
+          d.inq[(uint32_t)L.cw0[x] & ~TRACK_BIT] = 0;
+        if (blockIdx.x == 0 && threadIdx.x < NB) {
+          for (int q = 0; q < 3; q++) { wlc[NB * q + threadIdx.x] = 0; qc[NB * q + threadIdx.x] = 0; }
+          rlc[threadIdx.x] = 0;
+          if (threadIdx.x < 6) ctl->fs[threadIdx.x] = 0;
+          if (threadIdx.x < 2) { ctl->mu[threadIdx.x] = 0; ctl->gtop[threadIdx.x] = 0; }
+        }
+        if (blockIdx.x == 0 && d.local_gap)
+          for (int i = threadIdx.x; i < 2 * GAPW; i += NT) d.cnt[i] = 0;
+        gsync(d, grid, sm);
+        return -1;
+      }
       if (total(w0) == 0) break;                  // no active vertex: converged (R9)
     }
    }
@@ -1918,6 +1956,7 @@ __device__ void device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseC
       clk.lap(d, sm, ST_T_RIE, iter, 0, total(rc), rc[3]);
     }
   }
+  return 0;
 }
 
 // Binary search of v in the sorted row of u; -1 if absent.
@@ -1962,7 +2001,7 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(const __grid_con
     // (the final labels' histogram, see the PP epilogue); every other call rebuilds
     // them from its first RESET.  Published by the first grid barrier.
     if (!(mode == MODE_PP && d.warm)) for (int i = threadIdx.x; i < 2 * GAPW; i += NTHREADS) d.cnt[i] = 0;
-    if (mode == MODE_PP) for (int i = threadIdx.x; i < 2 * GAPW; i += NTHREADS) d.cnt_next[i] = 0;
+    if (mode == MODE_PP || mode == MODE_MINCUT) for (int i = threadIdx.x; i < 2 * GAPW; i += NTHREADS) d.cnt_next[i] = 0;
   }
   __syncthreads();
   const int32_t n = d.n;
@@ -2113,7 +2152,47 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(const __grid_con
   } else if (mode == MODE_PP) {
     // ---- stage 1: push on T || pull on S (Alg.8 l.15-28)
     clk.lap(d, sm, ST_T_PRO);
-    device_loop(d, grid, sm, clk, RK_PP, true, false, d.warm != 0);
+    // Warm start: discharge on the previous labels, then the universal certificate
+    // (R9).  When it holds, the state is converged and Alg.8's remaining work (the
+    // two-track BFS, P, stage 2) has nothing to change; the partition is the
+    // certificate's reach (R15) and S_min is left to dmf_min_cut_source_side.
+    const int lz = (d.warm && d.lazy) ? device_loop(d, grid, sm, clk, RK_PP, true, false, true, true) : 0;
+    if (lz == 1) {
+      long long f = 0;
+      int32_t *hist = sm.cand;
+      const bool want_hist = d.local_gap && d.cnt_next;
+      if (want_hist) {
+        for (int i = threadIdx.x; i < 2 * GAPW; i += NTHREADS) hist[i] = 0;
+        __syncthreads();
+      }
+      for (int32_t v = gt; v < n; v += nt) {
+        const long long ev = ldv(d.e + v);
+        f += v == d.t ? ev : (v != d.s && ev < 0 ? ev : 0);
+        const int32_t hpv = ldv(d.hp + v);
+        int32_t hmv = ldv(d.hm + v);
+        const bool tside = hpv < n;                // reaches t or a deficit: T' (R15)
+        d.part[v] = tside ? PART_T : PART_S;
+        if (tside) { d.hm[v] = n + 1; hmv = n + 1; }
+        else {
+          d.hp[v] = n + 1;
+          if (hmv > n) { d.hm[v] = n; hmv = n; }  // (T -> S': in the pull region, unreached)
+        }
+        if (want_hist) {
+          if (hpv < n && hpv < GAPW) atomicAdd(hist + hpv, 1);
+          if (hmv < n && hmv < GAPW) atomicAdd(hist + GAPW + hmv, 1);
+        }
+      }
+      f = bg.sum(f);
+      if (threadIdx.x == 0 && f) atomicAdd(reinterpret_cast<unsigned long long *>(&ctl->flow), (unsigned long long)f);
+      if (blockIdx.x == 0 && threadIdx.x == 0) ctl->lazy_ok = 1;
+      if (want_hist) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < 2 * GAPW; i += NTHREADS)
+          if (hist[i]) atomicAdd(d.cnt_next + i, hist[i]);
+      }
+    } else {
+    // (certificate failed after the warm iteration: the full stage 1 from fresh labels)
+    device_loop(d, grid, sm, clk, RK_PP, true, false, d.warm != 0 && lz == 0);
     // ---- P = {h+ = |V| and h- = |V|} (Alg.8 l.29-33), vertices with slots only
     if (blockIdx.x == 0 && threadIdx.x < NB) {
       ctl->qc[threadIdx.x] = 0;
@@ -2157,16 +2236,18 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(const __grid_con
     cta_snap(sm, 2, [&](int k) { return (long long)ldv(k ? &ctl->pexc : &ctl->pdef); });
     const bool has_def = sm.cv[0] > 0, has_exc = sm.cv[1] > 0;
     if (threadIdx.x == 0 && blockIdx.x == 0) sstat_add(sm, ST_S2_V, (unsigned long long)pc);
-    // ---- stage 2: Dynamic Push-Relabel restricted to P (Alg.8 l.34).  Its active
-    //      vertices are P's excess vertices and its roots P's deficits: with either set
-    //      empty its first global relabel would end the loop at once, so it is skipped.
+    // ---- stage 2: Dynamic Push-Relabel restricted to P (Alg.8 l.34).  Its roots are
+    //      P's deficits: without any, its first global relabel ends the loop at once and
+    //      reaches no P vertex (all of P goes to S'), so it is skipped.  With deficits
+    //      but no excess it still runs: its final BFS decides which P vertices go to T'.
     clk.lap(d, sm, ST_T_EPI);
+    if (pc > 0 && has_def) device_loop(d, grid, sm, clk, RK_STAGE2, true, true);
+    else if (pc > 0 && blockIdx.x == 0 && threadIdx.x == 0) sstat_add(sm, ST_S2_SKIP, 1);
     if (pc > 0 && has_exc) {
-      if (has_def) device_loop(d, grid, sm, clk, RK_STAGE2, true, true);
-      else if (blockIdx.x == 0 && threadIdx.x == 0) sstat_add(sm, ST_S2_SKIP, 1);
       // ---- S_min (R19) = stage 1's final forward reach from {s} u Exc_S (h- < |V|)
       //      united with the forward reach, inside P, of the excess left in P: no
-      //      residual edge enters P from S\P or leaves P towards T\P
+      //      residual edge enters P from S\P or leaves P towards T\P.
+      //      (Stage 2 moves excess only inside P and never creates any where P had none.)
       if (blockIdx.x == 0 && threadIdx.x < NB) {
         ctl->qc[threadIdx.x] = 0;
         if (threadIdx.x < 2) { ctl->fs[threadIdx.x] = 0; ctl->mu[threadIdx.x] = 0; }
@@ -2174,7 +2255,7 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(const __grid_con
       gsync(d, grid, sm);
       device_loop(d, grid, sm, clk, RK_MINCUT_P, false, false);
     } else if (pc > 0 && blockIdx.x == 0 && threadIdx.x == 0) {
-      sstat_add(sm, ST_S2_SKIP, 2);              // no excess in P: no stage-2 work and no P-reach
+      sstat_add(sm, ST_S2_SKIP, 1);              // no excess in P: its forward reach is empty
     }
     // ---- relabel partitions (Alg.8 l.35-49) and F (= sum over T' of e, R8)
     for (int32_t x = gt; x < pc; x += nt) {     // (+ the region encoding of the next warm start:
@@ -2209,6 +2290,7 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(const __grid_con
       for (int i = threadIdx.x; i < 2 * GAPW; i += NTHREADS)
         if (hist[i]) atomicAdd(d.cnt_next + i, hist[i]);
     }
+    }   // full stage 1
   } else if (mode == MODE_FLOW) {
     // Stage (ii): turn the converged pseudoflow into a
     // true maximum flow.  Every vertex with excess reaches s in the residual graph
@@ -2233,8 +2315,28 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(const __grid_con
     if (threadIdx.x == 0 && f) atomicAdd(reinterpret_cast<unsigned long long *>(&ctl->flow), (unsigned long long)f);
   } else if (mode == MODE_MINCUT || mode == MODE_MAXCUT) {
     device_loop(d, grid, sm, clk, mode == MODE_MINCUT ? RK_MINCUT : RK_MAXCUT, false, false);
-    for (int32_t v = gt; v < n; v += nt)
-      d.mask[v] = mode == MODE_MINCUT ? (ldv(d.hm + v) < n ? 1 : 0) : (ldv(d.hp + v) < n ? 0 : 1);
+    // MINCUT rewrites h- with the exact forward distances from {s} u Exc: the pull
+    // labels of a following DYN_PP warm start, with their level histogram
+    int32_t *hist = sm.cand;
+    const bool want_hist = mode == MODE_MINCUT && d.local_gap && d.cnt_next;
+    if (want_hist) {
+      for (int i = threadIdx.x; i < 2 * GAPW; i += NTHREADS) hist[i] = 0;
+      __syncthreads();
+    }
+    for (int32_t v = gt; v < n; v += nt) {
+      const int32_t hmv = ldv(d.hm + v);
+      d.mask[v] = mode == MODE_MINCUT ? (hmv < n ? 1 : 0) : (ldv(d.hp + v) < n ? 0 : 1);
+      if (want_hist) {
+        const int32_t hpv = ldv(d.hp + v);
+        if (hpv < n && hpv < GAPW) atomicAdd(hist + hpv, 1);
+        if (hmv < n && hmv < GAPW) atomicAdd(hist + GAPW + hmv, 1);
+      }
+    }
+    if (want_hist) {
+      __syncthreads();
+      for (int i = threadIdx.x; i < 2 * GAPW; i += NTHREADS)
+        if (hist[i]) atomicAdd(d.cnt_next + i, hist[i]);
+    }
   }
   clk.lap(d, sm, ST_T_EPI);
   __syncthreads();

@@ -63,6 +63,7 @@ KNOB_SETS = {
     "auto_topo_switch": dict(schedule="auto", topo_div=1000000),     # any active vertex -> topology phase
     "no_gap": dict(local_gap=-1),
     "no_warm": dict(warm=-1),
+    "no_certify": dict(certify=-1),
     "budget_stop_async": dict(schedule="async", budget_mul=-1000000, tail_items=1),
     "budget_stop_rounds": dict(schedule="rounds", budget_mul=-1000000),
     "budget_stop_topology": dict(schedule="topology", budget_mul=-1000000),
@@ -135,20 +136,33 @@ def test_grid_and_bipartite_schedules(dmf, name):
 
 def test_local_gap_fires_and_is_result_neutral(dmf):
     """The local gap exit is actually exercised (levels found empty, discharges parked)
-    on the bipartite recipe and changes nothing in F / S_min / S_max."""
-    g = W.bipartite(L=1 << 12, draws=1 << 16, seed=4)
-    res = {}
-    for gap in (0, -1):
-        f = dmf.DynMaxFlow.from_graph(g, local_gap=gap)
-        f.static_solve()
-        s = f.stats()
-        res[gap] = (f.flow_value(), f.min_cut_source_side().copy(), f.max_cut_source_side().copy(),
-                    s["gap_levels"], s["gap_skips"])
-        f.close()
-    assert res[0][0] == res[-1][0]
-    assert np.array_equal(res[0][1], res[-1][1]) and np.array_equal(res[0][2], res[-1][2])
-    assert res[0][3] > 0, "no emptied level was detected on the bipartite static solve"
-    assert res[-1][3] == 0 and res[-1][4] == 0
+    -- an asynchronous static solve and PP batches on RMAT-12/13 -- and changes nothing
+    in F / S_min / S_max."""
+    fired = 0
+    for scale in (12, 13):
+        g = W.rmat(scale, 16, 1, 7)
+        res = {}
+        for gap in (0, -1):
+            f = dmf.DynMaxFlow.from_graph(g, local_gap=gap, schedule="async")
+            f.static_solve()
+            s = f.stats()
+            out = [(f.flow_value(), f.min_cut_source_side().copy(), f.max_cut_source_side().copy())]
+            lv, sk = s["gap_levels"], s["gap_skips"]
+            st = W.CapState(g)
+            for j in range(4):
+                b = W.rmat_batch(g, st, 0.01, 800 + j)
+                st.apply(b)
+                f.apply_batch(b.u, b.v, b.new_cap, algo="pp")
+                s = f.stats()
+                lv += s["gap_levels"]; sk += s["gap_skips"]
+                out.append((f.flow_value(), f.min_cut_source_side().copy(), f.max_cut_source_side().copy()))
+            res[gap] = (out, lv, sk)
+            f.close()
+        for a, b in zip(res[0][0], res[-1][0]):
+            assert a[0] == b[0] and np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
+        assert res[-1][1] == 0 and res[-1][2] == 0
+        fired += res[0][1]
+    assert fired > 0, "no emptied level was detected"
 
 
 # ------------------------------------------------------------------ failure / state paths

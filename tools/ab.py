@@ -27,16 +27,23 @@ for rep in range(2):
         f = P.DynMaxFlow.from_graph(g, **kn)
         f.static_solve(); st0 = f.stats()
         f.static_solve_pp(); st1 = f.stats()
-        per = []
+        per = []; cut = []
+        import torch
+        mask = torch.empty(g.n, dtype=torch.uint8, device="cuda")
         for j, b in enumerate(batches):
             f.apply_batch(b.u, b.v, b.new_cap, algo="pp")
             if j >= 5:
                 per.append(f.stats())
+            if not os.environ.get("AB_NO_CUT"):
+                t0 = time.perf_counter()
+                f.min_cut_source_side(mask)
+                if j >= 5:
+                    cut.append(1e3 * (time.perf_counter() - t0))
         ms = [p["device_ms"] for p in per]
         med = {k: round(float(np.median([p[k] for p in per])), 1) for k in keys}
         ex = {k: float(np.mean([p[k] for p in per])) for k in ("iterations", "gap_levels", "gap_skips", "tail_stops",
-                                                                 "budget_stops", "stage2_skipped", "discharge_vertices")}
-        print(f"{name:14s} rep{rep} batch ms p50={np.median(ms):.3f} p90={np.percentile(ms, 90):.3f} mean={np.mean(ms):.3f} "
+                                                                 "budget_stops", "stage2_skipped", "discharge_vertices", "certified")}
+        print(f"{name:14s} rep{rep} cut ms p50={np.median(cut) if cut else 0:.3f} batch ms p50={np.median(ms):.3f} p90={np.percentile(ms, 90):.3f} mean={np.mean(ms):.3f} "
               f"static alg1={st0['device_ms']:.2f} pp={st1['device_ms']:.2f}  {med}  {json.dumps({k: round(v, 2) for k, v in ex.items()})}",
               flush=True)
         f.close()

@@ -71,6 +71,15 @@ for r, tt in zip(cl, ts[R[:, 0] == 203]):
 if waits:
     w = np.array(waits)
     print(f"enqueue->claim wait: n={len(w)} p50={np.median(w):.2f} p90={np.percentile(w,90):.2f} max={w.max():.1f} us")
+lab = f.export_labels()
+vs, cnts = np.unique(items[:, 2].astype(np.int64), return_counts=True)
+o = np.argsort(-cnts)[:15]
+print("top vertices by items: (v, items, deg, part, e-sign, hp, hm)")
+ex = f.export_state()["e"]
+for i in o:
+    v = vs[i]
+    print(f"   v={v} items={cnts[i]} deg={deg[v]} part={lab['part'][v]} e={ex[v]} hp={lab['hp'][v]} hm={lab['hm'][v]} s={v == g.s} t={v == g.t}")
+print("distinct vertices", len(vs), "chunk vertices", len(np.unique(items[items[:, 3] == 204, 2])))
 edges = np.arange(0, ts.max() + 10, 10)
 for lo in edges:
     hi = lo + 10
