@@ -79,12 +79,15 @@ struct dmf_graph {
   int32_t topo_div = 16;
   int32_t check_level = 0;
   int32_t lazy = 1;          // DYN_PP warm start certified by the universal backward BFS
+  int32_t dmaxch = 0;        // DMF_DMAXCH: chunk items per big-vertex discharge activation (0: CH slots each)
   long long budget_mul = 1;
   int32_t *cnt = nullptr, *cnt_next = nullptr;   // local-gap level counts (this call / next warm call)
   int32_t *chk = nullptr;                          // invariant check scratch (64 bytes)
   long long *e = nullptr;
   uint8_t *part = nullptr, *mask = nullptr, *rlf = nullptr;
-  int32_t *bbuf = nullptr;   // batch staging: u, v, c, slot  (4 * bcap)
+  int32_t *bbuf = nullptr;   // batch staging: u, v, c, slot, 3 undo records  (7 * bcap)
+  int2 *htab = nullptr;      // (u,v) -> slot table
+  int32_t hmask = 0;
   int64_t bcap = 0;
   Ctl *ctl = nullptr;
   Ctl *hctl = nullptr;       // pinned mirror
@@ -196,6 +199,17 @@ __global__ void k_slots(int32_t n, int64_t S, const unsigned long long *ukey, co
   }
 }
 
+// (u,v) -> slot table for O(1) batch lookups (linear probing; entry {v, slot}).
+__global__ void k_hash_insert(int64_t S, int32_t n, const unsigned long long *ukey, int2 *htab, uint32_t hmask) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < S; i += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long k = ukey[i];
+    const int32_t u = (int32_t)(k / (unsigned long long)n), v = (int32_t)(k % (unsigned long long)n);
+    const unsigned long long ent = ((unsigned long long)(uint32_t)i << 32) | (uint32_t)v;
+    for (uint32_t h = slot_hash(u, v) & hmask;; h = (h + 1) & hmask)
+      if (atomicCAS(reinterpret_cast<unsigned long long *>(htab + h), ~0ull, ent) == ~0ull) break;
+  }
+}
+
 __global__ void k_init_state(int64_t S, int32_t n, const int32_t *rev, const int32_t *cap, int32_t *res,
                              int32_t *rres, int32_t *stamp, long long *e, uint8_t *part, int32_t *hp, int32_t *hm) {
   const int64_t st = (int64_t)gridDim.x * blockDim.x;
@@ -287,7 +301,9 @@ static Dev make_dev(dmf_graph *g) {
   d.local_gap = g->local_gap; d.topo_div = g->topo_div; d.tail_items = g->tail_items;
   d.check_level = g->check_level;
   d.lazy = g->lazy;
+  d.dmaxch = g->dmaxch;
   d.plist = g->plist; d.stamp = g->stamp;
+  d.htab = g->htab; d.hmask = g->hmask;
   d.mask = g->mask; d.ctl = g->ctl;
   d.dbg = g->ddbg;
   d.trace = g->trace;
@@ -604,6 +620,7 @@ int dmf_create(int32_t n, const int64_t *row_ptr, const int32_t *col, const int3
     const int32_t td = knob(o.topo_div, "DMF_TOPO_DIV");
     g->topo_div = sched == DMF_SCHED_TOPOLOGY ? 0x3fffffff : (td == 0 ? 16 : (td < 0 ? 0 : td));
     g->lazy = knob(o.certify, "DMF_CERTIFY") < 0 ? 0 : 1;
+    if (const char *mc = getenv("DMF_DMAXCH")) g->dmaxch = atoi(mc) > 0 ? atoi(mc) : 0;
     g->check_level = knob(o.check_level, "DMF_CHECK_LEVEL");
     if (const char *ba = getenv("DMF_BU_ALPHA")) g->bu_alpha = atoi(ba) > 0 ? atoi(ba) : g->bu_alpha;
     if (const char *dd = getenv("DMF_DENSE_DIV")) g->dense_div = atoi(dd) > 0 ? atoi(dd) : g->dense_div;
@@ -628,9 +645,19 @@ int dmf_create(int32_t n, const int64_t *row_ptr, const int32_t *col, const int3
   CKB(cudaMemsetAsync(g->dcnt, 0, nn * 4, st));
   CKB(cudaMemsetAsync(g->dmin, 0x7f, nn * 4, st));   // DMIN_NONE
   CKB(cudaMemsetAsync(g->aq, 0xff, ((size_t)g->aq_mask + 1) * 8, st));   // AQ_EMPTY
+  {
+    if (S > (1LL << 30)) { fail(DMF_EOVERFLOW, "too many slots for the slot table (%lld > 2^30)", (long long)S); return bail(DMF_EOVERFLOW); }
+    size_t T = 1024;
+    while (T < 2 * (size_t)S) T <<= 1;
+    g->htab = (int2 *)g->alloc(T * sizeof(int2));
+    if (!g->htab) { fail(DMF_ENOMEM, "device allocation failed (slot table)"); return bail(DMF_ENOMEM); }
+    g->hmask = (int32_t)(T - 1);
+    CKB(cudaMemsetAsync(g->htab, 0xff, T * sizeof(int2), st));
+  }
   if (S) {
     CKB(cudaMemsetAsync(err, 0, 64, st));
     k_rows<<<blocks(nn + 1), TB, 0, st>>>(n, S, ukey, g->row);
+    k_hash_insert<<<blocks(S), TB, 0, st>>>(S, n, ukey, g->htab, (uint32_t)g->hmask);
     k_slots<<<blocks(S), TB, 0, st>>>(n, S, ukey, capsum, g->dst, g->rev, g->cap, err);
     unsigned long long *msum = (unsigned long long *)(err + 8);
     k_sum_i32<<<blocks(S), TB, 0, st>>>(S, isinput, msum);
@@ -700,7 +727,7 @@ int dmf_apply_batch(dmf_graph *g, int64_t k, const int32_t *u, const int32_t *v,
     if (k > g->bcap) {
       if (g->bbuf) g->release(g->bbuf);
       g->bcap = k + k / 4 + 1024;
-      g->bbuf = (int32_t *)g->alloc(4 * g->bcap * sizeof(int32_t));
+      g->bbuf = (int32_t *)g->alloc(7 * g->bcap * sizeof(int32_t));
       if (!g->bbuf) { g->bcap = 0; return fail(DMF_ENOMEM, "batch buffer allocation failed"); }
     }
     if (dev_in) { d.bu = u; d.bv = v; d.bc = new_cap; }
@@ -711,6 +738,7 @@ int dmf_apply_batch(dmf_graph *g, int64_t k, const int32_t *u, const int32_t *v,
       d.bu = g->bbuf; d.bv = g->bbuf + g->bcap; d.bc = g->bbuf + 2 * g->bcap;
     }
     d.bslot = g->bbuf + 3 * g->bcap;
+    d.brec = g->bbuf + 4 * g->bcap;
   }
   d.k = k;
   d.batch_id = ++g->batch_id;

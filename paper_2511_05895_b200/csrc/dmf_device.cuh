@@ -134,11 +134,15 @@ struct Dev {
   int32_t topo_div;          // topology-driven phase when > n / topo_div vertices are active (0: never)
   int32_t tail_items;        // async progress stop (<= 0: off)
   int32_t check_level;
+  int32_t dmaxch;            // discharge: at most this many chunk items per big-vertex activation (0: CH-slot chunks)
   int32_t lazy;              // DYN_PP warm start: certify with the universal backward BFS (no pull BFS / stage 2)
   int32_t *plist;            // region P of push-pull stage 2
   int32_t *stamp;            // per-slot batch stamp (duplicate detection)
   const int32_t *bu, *bv, *bc;  // batch entries
   int32_t *bslot;            // slot of each batch entry
+  int32_t *brec;             // per batch entry: residual delta, clamp, S->T saturation (undo of an invalid batch)
+  const int2 *htab;          // (u,v) -> slot table {v, slot}, {-1,-1} empty
+  int32_t hmask;
   uint8_t *mask;             // cut output
   Ctl *ctl;
   volatile int32_t *dbg;     // mapped pinned host words: progress beacon for the host watchdog

@@ -176,6 +176,20 @@ __device__ __forceinline__ int bin_of(const Dev &d, int32_t v) {
 // hub rows are spread over the whole grid (edge-balanced work units).
 constexpr int32_t CH = 512;
 
+// Discharge chunks of a big vertex: CH slots each, but at most dmaxch chunks per
+// activation (then bigger chunks, multiples of 128 slots) when dmaxch > 0.  A hub
+// re-activated many times then costs a bounded number of ring items per activation.
+__device__ __forceinline__ int32_t dis_csize(const Dev &d, int32_t deg) {
+  if (d.dmaxch <= 0) return CH;
+  int32_t c = (deg + d.dmaxch - 1) / d.dmaxch;
+  c = (c + 127) & ~127;
+  return c < CH ? CH : c;
+}
+__device__ __forceinline__ int32_t dis_nch(const Dev &d, int32_t deg) {
+  const int32_t c = dis_csize(d, deg);
+  return (deg + c - 1) / c;
+}
+
 struct BL {
   int32_t *buf;   // bin b at buf + b*n
   int32_t *c;
@@ -209,11 +223,11 @@ __device__ __forceinline__ void bl_append_conv(const Dev &d, const BL &bl, bool 
     warp_append(bin == 3, (int32_t)((uint32_t)v | tag), bl.bin(3), bl.c + 3);
   }
 }
-__device__ __forceinline__ void bl_append_one(const Dev &d, const BL &bl, int32_t v, uint32_t tag) {
+__device__ __forceinline__ void bl_append_one(const Dev &d, const BL &bl, int32_t v, uint32_t tag, bool dis = false) {
   const int32_t deg = d.row[v + 1] - d.row[v];
   const int bin = deg <= BIN0_MAX ? 0 : (deg <= BIN1_MAX ? 1 : (deg <= BIN2_MAX ? 2 : 3));
   if (bin >= 2 && bl.cq) {
-    const int32_t nch = (deg + CH - 1) / CH;
+    const int32_t nch = dis ? dis_nch(d, deg) : (deg + CH - 1) / CH;
     const int32_t pos = atomicAdd(bl.c + 3, nch);
     for (int32_t k = 0; k < nch; k++) bl.cq[pos + k] = chunk_entry(v, tag, k);
     return;
@@ -355,7 +369,7 @@ __device__ __forceinline__ void dbg_rec(const Dev &d, int32_t kind, int32_t a, i
 // can never finish an item before it is counted.
 __device__ __forceinline__ void async_enqueue(const Dev &d, int32_t v, uint32_t tag) {
   const int32_t deg = d.row[v + 1] - d.row[v];
-  const int32_t nch = deg > BIN1_MAX ? (deg + CH - 1) / CH : 1;
+  const int32_t nch = deg > BIN1_MAX ? dis_nch(d, deg) : 1;
   const unsigned long long old = atomicAdd(&d.ctl->aw, ((unsigned long long)nch << 32) | (unsigned long long)nch);
   const uint32_t pos = (uint32_t)(old >> 32);
   DBG(d, 202, v, (int32_t)pos, (int32_t)(uint32_t)old, nch);
@@ -376,7 +390,7 @@ __device__ __forceinline__ void activate(const Dev &d, const Track &k, const BL 
   if (sm.amode && ring) { async_enqueue(d, v, tag); return; }
   const int32_t pos = atomicAdd(&sm.acnt, 1);
   if (pos < ACAP) act_buf(sm)[pos] = (int32_t)((uint32_t)v | tag);
-  else bl_append_one(d, nxt, v, tag);
+  else bl_append_one(d, nxt, v, tag, true);
 }
 // One push of d on slot i = (u,v) of track k (ri = rev[i]): the four residual updates and
 // e(v) += d are fire-and-forget reductions; v is staged as an activation CANDIDATE that
@@ -512,9 +526,9 @@ __device__ __forceinline__ int wl_bin(int32_t deg) {
 
 // warp-convergent: every lane with pred appends ceil(deg/CH) chunk entries of v to bl's
 // chunk queue (count in bl.c[3]); one global atomic per warp
-__device__ __forceinline__ void chunks_conv(const BL &bl, bool pred, int32_t deg, int32_t v, uint32_t tag) {
+__device__ __forceinline__ void chunks_conv(const Dev &d, const BL &bl, bool pred, int32_t deg, int32_t v, uint32_t tag) {
   if (__ballot_sync(0xffffffffu, pred) == 0) return;
-  const int32_t nch = pred ? (deg + CH - 1) / CH : 0;
+  const int32_t nch = pred ? dis_nch(d, deg) : 0;
   WarpG g{(int)(threadIdx.x & 31)};
   long long tot;
   const int32_t ex = (int32_t)g.exscan(nch, tot);
@@ -548,7 +562,7 @@ __device__ __forceinline__ void claim_push(const Dev &d, Stage &st, const BfsCtx
     if (act) d.inq[v] = 1;
     stage_conv(st, 2, c.wl.bin(0), c.wl.c, wb == 0, val);
     stage_conv(st, 3, c.wl.bin(1), c.wl.c + 1, wb == 1, val);
-    chunks_conv(c.wl, wb >= 2, deg, v, tr ? TRACK_BIT : 0u);   // big rows: chunked discharge
+    chunks_conv(d, c.wl, wb >= 2, deg, v, tr ? TRACK_BIT : 0u);   // big rows: chunked discharge
   }
   if (claimed) fs.add(tr, deg);
   if (d.local_gap) {                // level counts of the local gap (R14 form 2)
@@ -580,7 +594,7 @@ __device__ __forceinline__ void claim_one(const Dev &d, Stage &st, const BfsCtx 
     const int wb = wl_bin(deg);
     if (wb < 2) stage_one(st, 2 + wb, c.wl.bin(wb), c.wl.c + wb, val);
     else {
-      const int32_t nch = (deg + CH - 1) / CH;
+      const int32_t nch = dis_nch(d, deg);
       const int32_t pos = atomicAdd(c.wl.c + 3, nch);
       for (int32_t k = 0; k < nch; k++) c.wl.cq[pos + k] = chunk_entry(v, tr ? TRACK_BIT : 0u, k);
     }
@@ -862,7 +876,7 @@ __device__ __forceinline__ void compact_domain(const Dev &d, TileSm &ts, int32_t
             if (wb == b) wo[j] = bs + __popc(m & ((1u << lane) - 1u));
           }
         }
-        const int32_t wch = wb == 2 ? (deg + CH - 1) / CH : 0;
+        const int32_t wch = wb == 2 ? dis_nch(d, deg) : 0;
         if (__ballot_sync(0xffffffffu, wch > 0)) {
           long long tot;
           const int32_t ex = (int32_t)g.exscan(wch, tot);
@@ -890,7 +904,7 @@ __device__ __forceinline__ void compact_domain(const Dev &d, TileSm &ts, int32_t
       if (wc[j] == 0 || wc[j] == 1) wl.bin(wc[j])[ts.base[3 + wc[j]] + wo[j]] = e;
       else if (wc[j] == 2) {
         const int32_t deg = d.row[vv[j] + 1] - d.row[vv[j]];
-        for (int32_t k = 0; k < (deg + CH - 1) / CH; k++) wl.cq[ts.base[5] + wo[j] + k] = chunk_entry(vv[j], tg[j], k);
+        for (int32_t k = 0; k < dis_nch(d, deg); k++) wl.cq[ts.base[5] + wo[j] + k] = chunk_entry(vv[j], tg[j], k);
       }
     }
     __syncthreads();
@@ -903,7 +917,8 @@ __device__ __forceinline__ int32_t *rel_buf(Smem &sm) { return &sm.st.w[0][0]; }
 // block-wide: move `cnt` staged entries (vertex | track tag) into the binned list bl
 // (bins 0/1, chunk entries for bigger rows when bl is chunked, else bins 2/3): one
 // global atomic per category per CTA.  Uses sm.ts; callers pass a block-uniform cnt.
-__device__ __forceinline__ void vflush(const Dev &d, TileSm &ts, const int32_t *buf, int32_t cnt, const BL &bl) {
+__device__ __forceinline__ void vflush(const Dev &d, TileSm &ts, const int32_t *buf, int32_t cnt, const BL &bl,
+                                       bool dis) {
   for (int32_t t0 = 0; t0 < cnt; t0 += NT) {
     if (threadIdx.x < 4) ts.cnt[threadIdx.x] = 0;
     __syncthreads();
@@ -914,7 +929,7 @@ __device__ __forceinline__ void vflush(const Dev &d, TileSm &ts, const int32_t *
       const int32_t v = (int32_t)((uint32_t)e & ~TRACK_BIT);
       const int32_t deg = d.row[v + 1] - d.row[v];
       cat = deg <= BIN0_MAX ? 0 : (deg <= BIN1_MAX ? 1 : (deg <= BIN2_MAX ? 2 : 3));
-      if (cat >= 2 && bl.cq) { cat = 3; nch = (deg + CH - 1) / CH; }
+      if (cat >= 2 && bl.cq) { cat = 3; nch = dis ? dis_nch(d, deg) : (deg + CH - 1) / CH; }
       off = atomicAdd(&ts.cnt[cat], nch ? nch : 1);
     }
     __syncthreads();
@@ -952,8 +967,8 @@ __device__ __forceinline__ void dis_flush(const Dev &d, Smem &sm, const BL &nxt,
   const int32_t a = min(sm.acnt, ACAP), r = min(sm.rcnt, RCAP);
   __syncthreads();
   if (threadIdx.x == 0) { sm.acnt = 0; sm.rcnt = 0; }
-  vflush(d, sm.ts, act_buf(sm), a, nxt);
-  vflush(d, sm.ts, rel_buf(sm), r, rl);
+  vflush(d, sm.ts, act_buf(sm), a, nxt, true);
+  vflush(d, sm.ts, rel_buf(sm), r, rl, false);
 }
 
 // block-wide: flush the stages and publish the per-CTA frontier slot sums and the
@@ -1196,9 +1211,10 @@ __device__ __forceinline__ void discharge_chunk(const Dev &d, Smem &sm, long lon
   const Track k = make_track(d, tr);
   const int32_t n = d.n;
   const int32_t rbeg = d.row[u], rend = d.row[u + 1];
-  const int32_t beg = rbeg + (int32_t)(ce >> 32) * CH;
-  const int32_t end = min(rend, beg + CH);
-  const int32_t nch = (rend - rbeg + CH - 1) / CH;
+  const int32_t csz = dis_csize(d, rend - rbeg);
+  const int32_t beg = rbeg + (int32_t)(ce >> 32) * csz;
+  const int32_t end = min(rend, beg + csz);
+  const int32_t nch = (rend - rbeg + csz - 1) / csz;
   const unsigned long long t_start = d.trace ? gtimer() : 0;
   const int32_t hu = ldv(k.hgt + u);
   if (lane == 0) DBG(d, 204, u, (int32_t)(ce >> 32), rend - rbeg, 0);
@@ -1351,21 +1367,28 @@ __device__ __forceinline__ void process_dis(const BL &bl, const int32_t c[NB], i
 __device__ __forceinline__ void rie_slots(const Dev &d, const Track &k, int32_t u, int32_t hu, int32_t i0, int32_t end,
                                           int32_t step, uint32_t tag, const BL &nxt, Smem &sm, long long &moved,
                                           unsigned long long &sat) {
-  for (int32_t i = i0; i < end; i += step) {
-    const int32_t r = ldv(k.F + i);
-    if (r > 0) {
-      const int32_t v = d.dst[i];
-      if (hu > ldl1(k.hgt + v) + 1) {            // heights are frozen in RIE
+  (void)nxt;                             // the next global relabel finds newly active vertices
+  for (int32_t b = i0; b < end; b += 4 * step) {
+    int32_t r[4], v[4], h[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) {        // independent loads first (ILP), then the gathers
+      const int32_t i = b + j * step;
+      r[j] = i < end ? ldv(k.F + i) : 0;
+      v[j] = i < end ? d.dst[i] : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; j++) h[j] = r[j] > 0 ? ldl1(k.hgt + v[j]) : 0x3fffffff;   // heights are frozen in RIE
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      if (r[j] > 0 && hu > h[j] + 1) {
+        const int32_t i = b + j * step;
         const int32_t ri = d.rev[i];
         k.F[i] = 0;
         k.R[ri] = 0;
-        atomicAdd(k.F + ri, r);
-        atomicAdd(k.R + i, r);
-        const long long old = (long long)atomicAdd(reinterpret_cast<unsigned long long *>(d.e + v),
-                                                   (unsigned long long)((long long)r * k.sign));
-        const long long eo = old * k.sign;
-        (void)eo; (void)nxt;             // the next global relabel finds newly active vertices
-        moved += r;
+        atomicAdd(k.F + ri, r[j]);
+        atomicAdd(k.R + i, r[j]);
+        atom_add(d.e + v[j], (long long)r[j] * k.sign);
+        moved += r[j];
         sat++;
       }
     }
@@ -1598,7 +1621,7 @@ __device__ __forceinline__ void topology_sweep(const Dev &d, Smem &sm, const int
         }
       }
     }
-    chunks_conv(tch, act && deg > BIN1_MAX, deg, v, (uint32_t)entry & TRACK_BIT);
+    chunks_conv(d, tch, act && deg > BIN1_MAX, deg, v, (uint32_t)entry & TRACK_BIT);
     if (act && deg <= BIN0_MAX) discharge(d, ThreadG{}, sm, entry, rl, tch, nullptr);
     __syncwarp();
     unsigned m = __ballot_sync(0xffffffffu, act && deg > BIN0_MAX && deg <= BIN1_MAX);
@@ -1959,15 +1982,21 @@ __device__ int device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseCl
   return 0;
 }
 
-// Binary search of v in the sorted row of u; -1 if absent.
+// Slot of (u,v), -1 if absent: open-addressing (u,v) -> slot table built by
+// dmf_create (linear probing, load <= 1/2); an entry {v, slot} matches when its slot
+// lies in u's row.  One 8-byte load per probe, probes of a run share a sector.
+__device__ __forceinline__ uint32_t slot_hash(int32_t u, int32_t v) {
+  unsigned long long k = ((unsigned long long)(uint32_t)u << 32) | (uint32_t)v;
+  k ^= k >> 33; k *= 0xff51afd7ed558ccdull; k ^= k >> 33; k *= 0xc4ceb9fe1a85ec53ull; k ^= k >> 33;
+  return (uint32_t)k;
+}
 __device__ __forceinline__ int32_t find_slot(const Dev &d, int32_t u, int32_t v) {
-  int32_t lo = d.row[u], hi = d.row[u + 1];
-  while (lo < hi) {
-    const int32_t mid = (lo + hi) >> 1;
-    const int32_t x = d.dst[mid];
-    if (x < v) lo = mid + 1; else hi = mid;
+  const int32_t lo = d.row[u], hi = d.row[u + 1];
+  for (uint32_t h = slot_hash(u, v) & (uint32_t)d.hmask;; h = (h + 1) & (uint32_t)d.hmask) {
+    const int2 e = __ldg(d.htab + h);
+    if (e.x == v && e.y >= lo && e.y < hi) return e.y;
+    if (e.x < 0) return -1;
   }
-  return (lo < d.row[u + 1] && d.dst[lo] == v) ? lo : -1;
 }
 
 __device__ __forceinline__ void set_status(const Dev &d, int32_t code, int32_t entry) {
@@ -2017,42 +2046,40 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(const __grid_con
     for (int32_t v = gt; v < n; v += nt) d.e[v] = 0;
     gsync(d, grid, sm);
   } else if (mode == MODE_PR || mode == MODE_PP) {
-    // ---- Updates Processing (Alg.5), validated first (R11)
-    for (int64_t j = gt; j < d.k; j += nt) {
-      const int32_t u = d.bu[j], v = d.bv[j], c = d.bc[j];
-      int32_t slot = -1;
-      if (u < 0 || u >= n || v < 0 || v >= n) set_status(d, -1, (int32_t)j);
-      else if (c < 0 || c > 1073741823) set_status(d, -7, (int32_t)j);
-      else if ((slot = find_slot(d, u, v)) < 0) set_status(d, -2, (int32_t)j);
-      else if (atomicExch(d.stamp + slot, d.batch_id) == d.batch_id) set_status(d, -3, (int32_t)j);
-      d.bslot[j] = slot;
-    }
-    gsync(d, grid, sm);
-    clk.lap(d, sm, ST_T_PRO, 0, 1, (int32_t)d.k);
-    if (cta_ld(sm, &ctl->status) != 0) mode = -1;   // all-or-nothing: state untouched
+    // ---- Updates Processing (Alg.5), all-or-nothing (R11), in ONE pass per entry:
+    // validate (ids, capacity, slot lookup in the (u,v) hash table, duplicate stamp)
+    // and apply optimistically, recording what was added.  Every update below is a
+    // commutative atomic add, so if any entry of the batch is invalid a second pass
+    // subtracts exactly what the first added and the state is byte-identical again.
     // Alg.5 l.1-3 (c_f += c' - c) and l.4-11 (a negative slot returns its excess flow:
-    // e(u) += d, e(v) -= d, R10) fused per entry: the clamp of slot i depends only on
-    // c_f(i) + delta_i (the entry of the reverse slot never changes c_f(i) unless it
-    // is the negative one, and a pair has at most one: their sum c'_i + c'_ri >= 0);
-    // all updates are commutative atomics.  DYN_PP also saturates a touched S->T slot
-    // here (Alg.8 l.10-13, R12): at a converged cut a T->S slot can never go negative,
-    // so nothing else changes such a slot in this phase.
+    // e(u) += d, e(v) -= d, R10) are fused per entry: the clamp of slot i depends only
+    // on c_f(i) + delta_i (the entry of the reverse slot never changes c_f(i) unless it
+    // is the negative one, and a pair has at most one: their sum c'_i + c'_ri >= 0).
+    // DYN_PP also saturates a touched S->T slot here (Alg.8 l.10-13, R12): at a
+    // converged cut a T->S slot can never go negative, so nothing else changes it.
     // e(s) / e(t) deltas are summed per CTA: batches are biased toward s-out and t-in
-    // slots (R20), so per-entry atomics would serialise on those two addresses
+    // slots (R20), so per-entry atomics would serialise on those two addresses.
     long long ds = 0, dt = 0;
     auto eadd = [&](int32_t x, long long delta) {
       if (x == d.s) ds += delta; else if (x == d.t) dt += delta; else atom_add(d.e + x, delta);
     };
-    for (int64_t j = gt; mode >= 0 && j < d.k; j += nt) {
-      const int32_t i = d.bslot[j];
+    for (int64_t j = gt; j < d.k; j += nt) {
+      const int32_t u = d.bu[j], v = d.bv[j], c = d.bc[j];
+      int32_t i = -1;
+      if (u < 0 || u >= n || v < 0 || v >= n) set_status(d, -1, (int32_t)j);
+      else if (c < 0 || c > 1073741823) set_status(d, -7, (int32_t)j);
+      else if ((i = find_slot(d, u, v)) < 0) set_status(d, -2, (int32_t)j);
+      else if (atomicExch(d.stamp + i, d.batch_id) == d.batch_id) set_status(d, -3, (int32_t)j);
+      d.bslot[j] = i;
+      if (i < 0) continue;
       const int32_t ri = d.rev[i];
-      const int32_t u = d.bu[j], v = d.bv[j];
-      const int32_t delta = d.bc[j] - d.cap[i];
-      d.cap[i] = d.bc[j];
+      const int32_t delta = c - ldv(d.cap + i);
+      atomicAdd(d.cap + i, delta);
       int32_t r = atomicAdd(d.res + i, delta) + delta;
       atomicAdd(d.rres + ri, delta);
+      int32_t dd = 0, sat = 0;
       if (r < 0) {                                 // flow on (u,v) above the new capacity
-        const int32_t dd = -r;
+        dd = -r;
         atomicAdd(d.res + i, dd);
         atomicAdd(d.rres + ri, dd);
         atomicAdd(d.res + ri, -dd);
@@ -2061,24 +2088,48 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(const __grid_con
         eadd(v, -(long long)dd);
         r = 0;
       }
-      if (mode == MODE_PP && r > 0 && d.part[u] == PART_S && d.part[v] == PART_T) {
-        atomicAdd(d.res + i, -r);                  // saturate the touched S->T slot
+      if (mode == MODE_PP && r > 0 && ldv(d.part + u) == PART_S && ldv(d.part + v) == PART_T) {
+        sat = r;                                   // saturate the touched S->T slot
+        atomicAdd(d.res + i, -r);
         atomicAdd(d.rres + ri, -r);
         atomicAdd(d.res + ri, r);
         atomicAdd(d.rres + i, r);
         eadd(v, (long long)r);
         eadd(u, -(long long)r);
       }
+      d.brec[3 * j] = delta; d.brec[3 * j + 1] = dd; d.brec[3 * j + 2] = sat;
     }
-    if (mode >= 0) {
-      ds = bg.sum(ds);
-      dt = bg.sum(dt);
+    auto flush_st = [&]() {
+      const long long a = bg.sum(ds), b = bg.sum(dt);
       if (threadIdx.x == 0) {
-        if (ds) atom_add(d.e + d.s, ds);
-        if (dt) atom_add(d.e + d.t, dt);
+        if (a) atom_add(d.e + d.s, a);
+        if (b) atom_add(d.e + d.t, b);
       }
+      ds = 0; dt = 0;
+    };
+    flush_st();
+    gsync(d, grid, sm);
+    clk.lap(d, sm, ST_T_PRO, 0, 1, (int32_t)d.k);
+    if (cta_ld(sm, &ctl->status) != 0) {           // an invalid entry: undo every applied one
+      mode = -1;
+      for (int64_t j = gt; j < d.k; j += nt) {
+        const int32_t i = d.bslot[j];
+        if (i < 0) continue;
+        const int32_t ri = d.rev[i];
+        const int32_t u = d.bu[j], v = d.bv[j];
+        const int32_t delta = d.brec[3 * j], dd = d.brec[3 * j + 1], sat = d.brec[3 * j + 2];
+        if (sat) {
+          atomicAdd(d.res + i, sat); atomicAdd(d.rres + ri, sat); atomicAdd(d.res + ri, -sat); atomicAdd(d.rres + i, -sat);
+          eadd(v, -(long long)sat); eadd(u, (long long)sat);
+        }
+        if (dd) {
+          atomicAdd(d.res + i, -dd); atomicAdd(d.rres + ri, -dd); atomicAdd(d.res + ri, dd); atomicAdd(d.rres + i, dd);
+          eadd(u, -(long long)dd); eadd(v, (long long)dd);
+        }
+        atomicAdd(d.res + i, -delta); atomicAdd(d.rres + ri, -delta); atomicAdd(d.cap + i, -delta);
+      }
+      flush_st();
       gsync(d, grid, sm);
-      clk.lap(d, sm, ST_T_PRO, 0, 2, (int32_t)d.k);
     }
     if (mode == MODE_PP && d.warm) {
       // Warm start of Alg.8 stage 1: only batch endpoints changed excess, so the
