@@ -65,7 +65,8 @@ struct dmf_graph {
   int32_t *hp = nullptr, *hm = nullptr, *q0 = nullptr, *q1 = nullptr, *wl = nullptr, *rl = nullptr;
   int32_t *plist = nullptr, *stamp = nullptr, *inq = nullptr, *bul = nullptr;
   long long *cq0 = nullptr, *cq1 = nullptr, *cqr = nullptr, *cw0 = nullptr, *cw1 = nullptr;
-  int32_t *dcnt = nullptr, *dmin = nullptr;
+  int32_t *dcnt = nullptr, *dmin = nullptr, *arc = nullptr;
+  bool probes = true;        // DMF_PROBE=0: big vertices always enqueue all their chunks
   long long *aq = nullptr;
   int32_t aq_mask = 0;
   // engine knobs, resolved from dmf_options (+ DMF_* environment overrides) in dmf_create
@@ -73,13 +74,14 @@ struct dmf_graph {
   bool async_static = false; // static solve from zero flow: rounds (massively parallel work)
   int32_t async_warps = 8;
   int32_t bu_alpha = (int32_t)BU_ALPHA, dense_div = (int32_t)DENSE_DIV;
-  int32_t async_sleep_ns = 1024;
+  int32_t async_sleep_ns = 128;
   int32_t tail_items = 2048;
   int32_t local_gap = 1;
   int32_t topo_div = 16;
   int32_t check_level = 0;
   int32_t lazy = 1;          // DYN_PP warm start certified by the universal backward BFS
-  int32_t dmaxch = 0;        // DMF_DMAXCH: chunk items per big-vertex discharge activation (0: CH slots each)
+  int32_t dmaxch = 0;
+  int32_t imm_act = 1;       // DMF_IMM_ACT=0: stage pushed heads and check them after the item        // DMF_DMAXCH: chunk items per big-vertex discharge activation (0: CH slots each)
   long long budget_mul = 1;
   int32_t *cnt = nullptr, *cnt_next = nullptr;   // local-gap level counts (this call / next warm call)
   int32_t *chk = nullptr;                          // invariant check scratch (64 bytes)
@@ -292,7 +294,7 @@ static Dev make_dev(dmf_graph *g) {
   d.q0 = g->q0; d.q1 = g->q1;
   d.wl = g->wl; d.rl = g->rl; d.inq = g->inq; d.bul = g->bul; d.rlf = g->rlf;
   d.cq0 = g->cq0; d.cq1 = g->cq1; d.cqr = g->cqr; d.cw0 = g->cw0; d.cw1 = g->cw1;
-  d.dcnt = g->dcnt; d.dmin = g->dmin;
+  d.dcnt = g->dcnt; d.dmin = g->dmin; d.arc = g->probes ? g->arc : nullptr;
   d.aq = g->aq; d.aq_mask = g->aq_mask; d.async = g->async ? 1 : 0;
   d.async_warps = g->async_warps;
   d.bu_alpha = g->bu_alpha; d.dense_div = g->dense_div;
@@ -302,6 +304,7 @@ static Dev make_dev(dmf_graph *g) {
   d.check_level = g->check_level;
   d.lazy = g->lazy;
   d.dmaxch = g->dmaxch;
+  d.imm_act = g->imm_act;
   d.plist = g->plist; d.stamp = g->stamp;
   d.htab = g->htab; d.hmask = g->hmask;
   d.mask = g->mask; d.ctl = g->ctl;
@@ -569,13 +572,15 @@ int dmf_create(int32_t n, const int64_t *row_ptr, const int32_t *col, const int3
   g->rlf = (uint8_t *)g->alloc(nn);
   g->bul = (int32_t *)g->alloc(2 * nn * 4);
   const size_t cqn = (size_t)(S / CH) + nn + 64;   // >= sum over vertices of ceil(deg / CH)
-  g->cq0 = (long long *)g->alloc(cqn * 8);
-  g->cq1 = (long long *)g->alloc(cqn * 8);
+  const size_t fqn = (size_t)(S / BCH) + nn + 64;  // >= sum over vertices of ceil(deg / BCH) (BFS frontier chunks)
+  g->cq0 = (long long *)g->alloc(fqn * 8);
+  g->cq1 = (long long *)g->alloc(fqn * 8);
   g->cqr = (long long *)g->alloc(cqn * 8);
   g->cw0 = (long long *)g->alloc(cqn * 8);
   g->cw1 = (long long *)g->alloc(cqn * 8);
   g->dcnt = (int32_t *)g->alloc(nn * 4);
   g->dmin = (int32_t *)g->alloc(nn * 4);
+  g->arc = (int32_t *)g->alloc(nn * 4);
   {
     // live ring window <= queued items (<= n + S/CH, inq-deduplicated) + one outstanding
     // claim per warp of the grid (idle warps claim ahead of the tail): no index aliases
@@ -589,7 +594,7 @@ int dmf_create(int32_t n, const int64_t *row_ptr, const int32_t *col, const int3
   g->ctl = (Ctl *)g->alloc(sizeof(Ctl));
   if (!g->row || !g->dst || !g->rev || !g->cap || !g->res || !g->rres || !g->stamp || !g->e || !g->hp || !g->hm ||
       !g->part || !g->mask || !g->q0 || !g->q1 || !g->wl || !g->rl || !g->plist || !g->ctl || !g->inq || !g->rlf || !g->bul || !g->cq0 || !g->cq1 || !g->cqr ||
-      !g->cw0 || !g->cw1 || !g->dcnt || !g->dmin || !g->aq) {
+      !g->cw0 || !g->cw1 || !g->dcnt || !g->dmin || !g->arc || !g->aq) {
     fail(DMF_ENOMEM, "device allocation failed (state, S=%lld)", (long long)S);
     return bail(DMF_ENOMEM);
   }
@@ -621,10 +626,12 @@ int dmf_create(int32_t n, const int64_t *row_ptr, const int32_t *col, const int3
     g->topo_div = sched == DMF_SCHED_TOPOLOGY ? 0x3fffffff : (td == 0 ? 16 : (td < 0 ? 0 : td));
     g->lazy = knob(o.certify, "DMF_CERTIFY") < 0 ? 0 : 1;
     if (const char *mc = getenv("DMF_DMAXCH")) g->dmaxch = atoi(mc) > 0 ? atoi(mc) : 0;
+    if (const char *pb = getenv("DMF_PROBE")) g->probes = atoi(pb) != 0;
+    if (const char *ia = getenv("DMF_IMM_ACT")) g->imm_act = atoi(ia) != 0;
     g->check_level = knob(o.check_level, "DMF_CHECK_LEVEL");
     if (const char *ba = getenv("DMF_BU_ALPHA")) g->bu_alpha = atoi(ba) > 0 ? atoi(ba) : g->bu_alpha;
     if (const char *dd = getenv("DMF_DENSE_DIV")) g->dense_div = atoi(dd) > 0 ? atoi(dd) : g->dense_div;
-    if (const char *sl = getenv("DMF_ASYNC_SLEEP_NS")) g->async_sleep_ns = atoi(sl) > 0 ? atoi(sl) : 1024;
+    if (const char *sl = getenv("DMF_ASYNC_SLEEP_NS")) g->async_sleep_ns = atoi(sl) > 0 ? atoi(sl) : 128;
     for (int i = 0; i < 7; i++)
       if (o.reserved[i]) { fail(DMF_EINVAL, "dmf_options.reserved must be zero"); return bail(DMF_EINVAL); }
   }
@@ -644,6 +651,7 @@ int dmf_create(int32_t n, const int64_t *row_ptr, const int32_t *col, const int3
   CKB(cudaMemsetAsync(g->rlf, 0, nn, st));
   CKB(cudaMemsetAsync(g->dcnt, 0, nn * 4, st));
   CKB(cudaMemsetAsync(g->dmin, 0x7f, nn * 4, st));   // DMIN_NONE
+  CKB(cudaMemsetAsync(g->arc, 0, nn * 4, st));
   CKB(cudaMemsetAsync(g->aq, 0xff, ((size_t)g->aq_mask + 1) * 8, st));   // AQ_EMPTY
   {
     if (S > (1LL << 30)) { fail(DMF_EOVERFLOW, "too many slots for the slot table (%lld > 2^30)", (long long)S); return bail(DMF_EOVERFLOW); }

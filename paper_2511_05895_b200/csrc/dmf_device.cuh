@@ -120,6 +120,7 @@ struct Dev {
   long long *cw0, *cw1;      // chunk queues of the discharge worklist ping-pong (vertices of > BIN1_MAX slots)
   int32_t *dcnt;             // chunked discharge: chunks of u finished in the current round
   int32_t *dmin;             // chunked discharge: lowest height among u's slots left residual (DMIN_NONE if none)
+  int32_t *arc;              // chunked discharge: current-arc chunk of u (the last chunk that pushed); NULL: no probes
   long long *aq;             // asynchronous discharge ring (AQ_EMPTY when free), aq_mask + 1 entries
   int32_t aq_mask;
   int32_t async;             // 1: asynchronous discharge phase, 0: barrier-separated rounds
@@ -134,6 +135,7 @@ struct Dev {
   int32_t topo_div;          // topology-driven phase when > n / topo_div vertices are active (0: never)
   int32_t tail_items;        // async progress stop (<= 0: off)
   int32_t check_level;
+  int32_t imm_act;           // async discharge: activate a pushed head at the push (returning atomic) instead of after the item
   int32_t dmaxch;            // discharge: at most this many chunk items per big-vertex activation (0: CH-slot chunks)
   int32_t lazy;              // DYN_PP warm start: certify with the universal backward BFS (no pull BFS / stage 2)
   int32_t *plist;            // region P of push-pull stage 2

@@ -164,6 +164,10 @@ __device__ __forceinline__ void gsync(const Dev &d, cg::grid_group &grid, Smem &
   if (d.trace_cta && threadIdx.x == 0) sm.tprev = gtimer();
 }
 
+// Global warp index, CTA-major: with few items they land on different SMs (each SM's
+// memory pipeline serves one dependent chain instead of sixteen).
+__device__ __forceinline__ int32_t gwarp_spread() { return (int32_t)((threadIdx.x >> 5) * gridDim.x + blockIdx.x); }
+
 __device__ __forceinline__ int bin_of(const Dev &d, int32_t v) {
   const int32_t deg = d.row[v + 1] - d.row[v];
   return deg <= BIN0_MAX ? 0 : (deg <= BIN1_MAX ? 1 : (deg <= BIN2_MAX ? 2 : 3));
@@ -175,6 +179,9 @@ __device__ __forceinline__ int bin_of(const Dev &d, int32_t v) {
 // entries in `cq` (count in c[3]), so that one warp takes one CH-slot chunk and
 // hub rows are spread over the whole grid (edge-balanced work units).
 constexpr int32_t CH = 512;
+// BFS frontier chunks of big rows: CH slots, or BCH (one warp-step each) in the small
+// certificate BFS of a DYN_PP warm start, whose levels are bound by latency, not scans
+constexpr int32_t BCH = 128;
 
 // Discharge chunks of a big vertex: CH slots each, but at most dmaxch chunks per
 // activation (then bigger chunks, multiples of 128 slots) when dmaxch > 0.  A hub
@@ -250,13 +257,13 @@ __device__ __forceinline__ void process_bl(const BL &bl, const int32_t c[NB], Sm
   {
     WarpG g{(int)(threadIdx.x & 31)};
     const int32_t *b = bl.bin(1);
-    const int32_t gw = blockIdx.x * WPB + (threadIdx.x >> 5), nw = gridDim.x * WPB;
+    const int32_t gw = gwarp_spread(), nw = gridDim.x * WPB;
     for (int32_t x = gw; x < c[1]; x += nw) fn(g, b[x]);
   }
   {
     TileG<8> g((int)(threadIdx.x & 31));
     const int32_t *b = bl.bin(0);
-    const int32_t gt = (blockIdx.x * NT + threadIdx.x) >> 3, nt = (gridDim.x * NT) >> 3;
+    const int32_t gt = (int32_t)((threadIdx.x >> 3) * gridDim.x + blockIdx.x), nt = (gridDim.x * NT) >> 3;
     for (int32_t x = gt; x < c[0]; x += nt) fn(g, b[x]);
   }
 }
@@ -283,7 +290,7 @@ __device__ __forceinline__ void process_bl_dyn(const BL &bl, const int32_t c[NB]
     WarpG g{(int)(threadIdx.x & 31)};
     const int32_t *b = bl.bin(1);
     const int32_t nw = gridDim.x * WPB;
-    int32_t x = blockIdx.x * WPB + (threadIdx.x >> 5);
+    int32_t x = gwarp_spread();
     while (x < c[1]) {
       fn(g, b[x]);
       if (g.lane == 0) x = nw + atomicAdd(cl + 1, 1);
@@ -294,7 +301,7 @@ __device__ __forceinline__ void process_bl_dyn(const BL &bl, const int32_t c[NB]
     TileG<8> g((int)(threadIdx.x & 31));
     const int32_t *b = bl.bin(0);
     const int32_t ntl = (gridDim.x * NT) >> 3;
-    int32_t x = (blockIdx.x * NT + threadIdx.x) >> 3;
+    int32_t x = (int32_t)((threadIdx.x >> 3) * gridDim.x + blockIdx.x);
     while (x < c[0]) {
       fn(g, b[x]);
       if (g.rank() == 0) x = ntl + atomicAdd(cl + 2, 1);
@@ -367,14 +374,27 @@ __device__ __forceinline__ void dbg_rec(const Dev &d, int32_t kind, int32_t a, i
 // Asynchronous discharge: append v (every CH-slot chunk of a big row) to the ring.  One
 // atomic reserves the ring positions AND counts the items as pending, so a consumer
 // can never finish an item before it is counted.
-__device__ __forceinline__ void async_enqueue(const Dev &d, int32_t v, uint32_t tag) {
-  const int32_t deg = d.row[v + 1] - d.row[v];
-  const int32_t nch = deg > BIN1_MAX ? dis_nch(d, deg) : 1;
+// A big vertex (> BIN1_MAX slots) activated through the ring first gets ONE probe item:
+// its current-arc chunk (the last chunk that pushed, d.arc).  Only if the probe leaves
+// excess does it enqueue all its chunks (enqueue_full).  A hub drained again and again
+// by its neighbours (pull track) is then re-served by one item, not by all its chunks.
+constexpr uint32_t PROBE_BIT = 0x40000000u;
+__device__ __forceinline__ void enqueue_items(const Dev &d, int32_t v, uint32_t tag, int32_t nch, uint32_t k0) {
   const unsigned long long old = atomicAdd(&d.ctl->aw, ((unsigned long long)nch << 32) | (unsigned long long)nch);
   const uint32_t pos = (uint32_t)(old >> 32);
   DBG(d, 202, v, (int32_t)pos, (int32_t)(uint32_t)old, nch);
   for (int32_t k = 0; k < nch; k++)
-    *(volatile long long *)(d.aq + ((pos + (uint32_t)k) & (uint32_t)d.aq_mask)) = chunk_entry(v, tag, k);
+    *(volatile long long *)(d.aq + ((pos + (uint32_t)k) & (uint32_t)d.aq_mask)) = chunk_entry(v, tag, (int32_t)(k0 + k));
+}
+__device__ __forceinline__ void async_enqueue(const Dev &d, int32_t v, uint32_t tag) {
+  const int32_t deg = d.row[v + 1] - d.row[v];
+  if (deg > BIN1_MAX && d.arc) {
+    const int32_t a = ldv(d.arc + v);
+    const int32_t nch = dis_nch(d, deg);
+    enqueue_items(d, v, tag, 1, PROBE_BIT | (uint32_t)(a < nch ? a : 0));
+    return;
+  }
+  enqueue_items(d, v, tag, deg > BIN1_MAX ? dis_nch(d, deg) : 1, 0u);
 }
 
 __device__ __forceinline__ void activate(const Dev &d, const Track &k, const BL &nxt, int32_t v, uint32_t tag,
@@ -414,6 +434,15 @@ __device__ __forceinline__ void push_slot(const Dev &d, const Track &k, const BL
   atomicSub(k.R + ri, take);         //   mirror
   atomicAdd(k.F + ri, take);         // c_f(v,u) += d
   atomicAdd(k.R + i, take);          //   mirror
+  if (sm.amode && d.imm_act) {
+    // asynchronous phase: the returning atomic tells whether e(v) crossed 0, and v is
+    // queued at once (the next warp sees e(v): the atomic is performed; a residual it
+    // reads before this push's reductions land is only lower, so it never pushes twice)
+    const long long eo = (long long)atomicAdd(reinterpret_cast<unsigned long long *>(d.e + v),
+                                              (unsigned long long)((long long)take * k.sign)) * k.sign;
+    if (eo <= 0 && eo + take > 0) activate(d, k, nxt, v, tag, sm);
+    return;
+  }
   // rounds: one list per CTA, checked at the round end; async: one list per warp,
   // checked after the warp's item (async_candidates)
   const int w = (int)(threadIdx.x >> 5);
@@ -451,6 +480,7 @@ constexpr int TILE_ITEMS = 4;                     // vertices per thread per com
 struct BfsCtx {
   int32_t lvl;
   int32_t tgt;                      // height the vertices labelled in this phase receive (lvl + 1; 0 in RESET)
+  int32_t bch;                      // frontier chunk size (CH or BCH)
   bool collect;
   uint32_t bu;                      // bit tr: bottom-up this level on track tr
   uint32_t dense;                   // bit tr: top-down by idempotent stores + compaction
@@ -540,15 +570,21 @@ __device__ __forceinline__ void chunks_conv(const Dev &d, const BL &bl, bool pre
 
 // warp-convergent: claimed vertex -> next frontier (+ worklist if active); counts
 // the claimed vertex's slots into fs[track]
+__device__ __forceinline__ void claim_push_deg(const Dev &d, Stage &st, const BfsCtx &c, bool claimed, bool act,
+                                               int32_t v, int tr, FS &fs, int32_t deg);
 __device__ __forceinline__ void claim_push(const Dev &d, Stage &st, const BfsCtx &c, bool claimed, bool act, int32_t v,
                                            int tr, FS &fs) {
-  const int32_t deg = claimed ? d.row[v + 1] - d.row[v] : 0;
+  claim_push_deg(d, st, c, claimed, act, v, tr, fs, claimed ? d.row[v + 1] - d.row[v] : 0);
+}
+// (deg = the claimed vertex's slot count, loaded by the caller)
+__device__ __forceinline__ void claim_push_deg(const Dev &d, Stage &st, const BfsCtx &c, bool claimed, bool act,
+                                               int32_t v, int tr, FS &fs, int32_t deg) {
   const int fb = claimed ? front_bin(deg) : -1;
   const int32_t val = (int32_t)((uint32_t)v | (tr ? TRACK_BIT : 0u));
   stage_conv(st, 0, c.next.bin(0), c.next.c, fb == 0, val);
   stage_conv(st, 1, c.next.bin(1), c.next.c + 1, fb == 1, val);
   if (__ballot_sync(0xffffffffu, fb == 2)) {          // big rows -> edge-balanced chunks
-    const int32_t nch = fb == 2 ? (deg + CH - 1) / CH : 0;
+    const int32_t nch = fb == 2 ? (deg + c.bch - 1) / c.bch : 0;
     WarpG g{(int)(threadIdx.x & 31)};
     long long tot;
     const int32_t ex = (int32_t)g.exscan(nch, tot);
@@ -585,7 +621,7 @@ __device__ __forceinline__ void claim_one(const Dev &d, Stage &st, const BfsCtx 
   const int fb = front_bin(deg);
   if (fb < 2) stage_one(st, fb, c.next.bin(fb), c.next.c + fb, val);
   else {
-    const int32_t nch = (deg + CH - 1) / CH;
+    const int32_t nch = (deg + c.bch - 1) / c.bch;
     const int32_t pos = atomicAdd(c.next.c + 3, nch);
     for (int32_t k = 0; k < nch; k++) c.next.cq[pos + k] = chunk_entry(v, tr ? TRACK_BIT : 0u, k);
   }
@@ -625,6 +661,41 @@ __device__ __forceinline__ void td_slot(const Dev &d, Stage &st, const BfsCtx &c
   claim_push(d, st, c, claimed, act, v, tr, fs);
 }
 
+// Four slots per lane (one warp-step of td_vertex_warp / td_chunk_warp): the height
+// gathers, the claiming CASes, the activity and degree loads of the four are each
+// issued together, so a step costs four dependent round trips instead of sixteen.
+// (tr4[j]: the track of element j; dense tracks label by stores and append nothing)
+__device__ __forceinline__ void td_slot4(const Dev &d, Stage &st, const BfsCtx &c, const int tr4[4],
+                                         const int32_t rb[4], const int32_t vv[4], FS &fs) {
+  bool ok[4], claimed[4], act[4], dn[4];
+  int32_t old[4], deg[4];
+  int32_t *hg[4];
+  long long ev[4];
+#pragma unroll
+  for (int j = 0; j < 4; j++) {
+    const Track k = make_track(d, tr4[j]);
+    hg[j] = k.hgt;
+    dn[j] = c.isdense(tr4[j]);
+    ok[j] = rb[j] > 0 && vv[j] != k.excl && ldl1(k.hgt + vv[j]) == d.n;   // stale n: the CAS decides
+  }
+#pragma unroll
+  for (int j = 0; j < 4; j++) if (dn[j] && ok[j]) hg[j][vv[j]] = c.lvl + 1;
+  if (__ballot_sync(0xffffffffu, !(dn[0] && dn[1] && dn[2] && dn[3])) == 0) return;   // all dense: compaction appends
+#pragma unroll
+  for (int j = 0; j < 4; j++) old[j] = (ok[j] && !dn[j]) ? atomicCAS(hg[j] + vv[j], d.n, c.lvl + 1) : -1;
+#pragma unroll
+  for (int j = 0; j < 4; j++) {
+    claimed[j] = ok[j] && !dn[j] && old[j] == d.n;
+    ev[j] = claimed[j] && c.collect ? ldv(d.e + vv[j]) : 0;
+    deg[j] = claimed[j] ? d.row[vv[j] + 1] - d.row[vv[j]] : 0;
+  }
+#pragma unroll
+  for (int j = 0; j < 4; j++) {
+    act[j] = claimed[j] && (tr4[j] ? ev[j] < 0 : ev[j] > 0);
+    claim_push_deg(d, st, c, claimed[j], act[j], vv[j], tr4[j], fs, deg[j]);
+  }
+}
+
 // warp per frontier vertex (bin 1): coalesced scan of its row, 4 slots per lane per step
 __device__ __forceinline__ void td_vertex_warp(const Dev &d, Smem &sm, Stage &st, int32_t entry, const BfsCtx &c,
                                                FS &fs) {
@@ -642,8 +713,8 @@ __device__ __forceinline__ void td_vertex_warp(const Dev &d, Smem &sm, Stage &st
       rb[j] = i < end ? ldv(B + i) : 0;
       vv[j] = i < end ? d.dst[i] : 0;
     }
-#pragma unroll
-    for (int j = 0; j < 4; j++) td_slot(d, st, c, tr, rb[j], vv[j], fs);
+    const int tr4[4] = {tr, tr, tr, tr};
+    td_slot4(d, st, c, tr4, rb, vv, fs);
   }
   if (lane == 0) {
     sstat_add(sm, ST_BFS_SLOTS, (unsigned long long)(end - beg));
@@ -659,8 +730,9 @@ __device__ __forceinline__ void td_chunk_warp(const Dev &d, Smem &sm, Stage &st,
   if (c.isbu(tr)) return;
   const int lane = threadIdx.x & 31;
   const int32_t w = (int32_t)(lo & ~TRACK_BIT);
-  const int32_t rb0 = d.row[w] + (int32_t)(ce >> 32) * CH;
-  const int32_t end = min(d.row[w + 1], rb0 + CH);
+  const unsigned long long t_start = d.trace ? gtimer() : 0;
+  const int32_t rb0 = d.row[w] + (int32_t)(ce >> 32) * c.bch;
+  const int32_t end = min(d.row[w + 1], rb0 + c.bch);
   const int32_t *B = make_track(d, tr).B;
   for (int32_t base = rb0; base < end; base += 128) {
     int32_t rb[4], vv[4];
@@ -670,10 +742,14 @@ __device__ __forceinline__ void td_chunk_warp(const Dev &d, Smem &sm, Stage &st,
       rb[j] = i < end ? ldv(B + i) : 0;
       vv[j] = i < end ? d.dst[i] : 0;
     }
-#pragma unroll
-    for (int j = 0; j < 4; j++) td_slot(d, st, c, tr, rb[j], vv[j], fs);
+    const int tr4[4] = {tr, tr, tr, tr};
+    td_slot4(d, st, c, tr4, rb, vv, fs);
   }
   if (lane == 0) sstat_add(sm, ST_BFS_SLOTS, (unsigned long long)(end - rb0));
+  if (d.trace && lane == 0) {           // slowest chunk of the level: (ns, vertex)
+    const unsigned long long dt = gtimer() - t_start;
+    atomicMax(&d.ctl->slow, (min(dt, 0xffffffffull) << 32) | (unsigned long long)(uint32_t)w);
+  }
 }
 
 // warp over up to 32 low-degree frontier vertices (bin 0): their rows are
@@ -694,22 +770,27 @@ __device__ __forceinline__ void td_small_chunk(const Dev &d, Smem &sm, Stage &st
   long long tot;
   const int32_t off = (int32_t)g.exscan(deg, tot);
   const int32_t total = (int32_t)tot;
-  for (int32_t t0 = 0; t0 < total; t0 += 32) {
-    const int32_t k = t0 + lane;
-    int j = 0;
+  for (int32_t t0 = 0; t0 < total; t0 += 128) {
+    int tr4[4];
+    int32_t rb[4], vv[4];
 #pragma unroll
-    for (int s = 16; s > 0; s >>= 1) {
-      const int32_t o = __shfl_sync(0xffffffffu, off, j + s);
-      if (o <= k) j += s;
+    for (int q = 0; q < 4; q++) {               // slots t0 + q*32 + lane: locate, then load
+      const int32_t k = t0 + q * 32 + lane;
+      int j = 0;
+#pragma unroll
+      for (int s = 16; s > 0; s >>= 1) {
+        const int32_t o = __shfl_sync(0xffffffffu, off, j + s);
+        if (o <= k) j += s;
+      }
+      const int32_t ej = __shfl_sync(0xffffffffu, entry, j);
+      const int32_t bj = __shfl_sync(0xffffffffu, beg, j);
+      const int32_t oj = __shfl_sync(0xffffffffu, off, j);
+      tr4[q] = ((uint32_t)ej & TRACK_BIT) ? 1 : 0;
+      const int32_t i = bj + (k - oj);
+      rb[q] = k < total ? ldv(make_track(d, tr4[q]).B + i) : 0;
+      vv[q] = k < total ? d.dst[i] : 0;
     }
-    const int32_t ej = __shfl_sync(0xffffffffu, entry, j);
-    const int32_t bj = __shfl_sync(0xffffffffu, beg, j);
-    const int32_t oj = __shfl_sync(0xffffffffu, off, j);
-    const int tr = ((uint32_t)ej & TRACK_BIT) ? 1 : 0;
-    const int32_t i = bj + (k - oj);
-    int32_t rb = 0, v = 0;
-    if (k < total) { rb = ldv(make_track(d, tr).B + i); v = d.dst[i]; }
-    td_slot(d, st, c, tr, rb, v, fs);
+    td_slot4(d, st, c, tr4, rb, vv, fs);
   }
   if (lane == 0) {
     sstat_add(sm, ST_BFS_SLOTS, (unsigned long long)total);
@@ -813,7 +894,8 @@ __device__ __forceinline__ void bfs_bottom_up_b(const Dev &d, const G &g, Smem &
 template <class Classify>
 __device__ __forceinline__ void compact_domain(const Dev &d, TileSm &ts, int32_t N, const int32_t *dom,
                                                const BL &next, const BL &wl, bool collect, Classify classify,
-                                               long long &fs0, long long &fs1, int32_t &nv0, int32_t &nv1) {
+                                               long long &fs0, long long &fs1, int32_t &nv0, int32_t &nv1,
+                                               int32_t bch) {
   const int lane = threadIdx.x & 31;
   const int32_t tile_sz = TILE_ITEMS * NT;
   WarpG g{lane};
@@ -854,7 +936,7 @@ __device__ __forceinline__ void compact_domain(const Dev &d, TileSm &ts, int32_t
         }
       }
       // frontier chunks
-      const int32_t nch = fb == 2 ? (deg + CH - 1) / CH : 0;
+      const int32_t nch = fb == 2 ? (deg + bch - 1) / bch : 0;
       nchv[j] = nch;
       if (__ballot_sync(0xffffffffu, nch > 0)) {
         long long tot;
@@ -996,11 +1078,19 @@ __device__ __forceinline__ void bfs_expand_level(const Dev &d, cg::grid_group &g
   FS fs;
   if (bu) bfs_bottom_up_a(d, sm, st, ctx, bul, bulc, fs);
   if (ctx.bu != 3u) {
-    const int32_t gw = blockIdx.x * WPB + (threadIdx.x >> 5), nw = gridDim.x * WPB;
-    for (int32_t x = gw; x < c[3]; x += nw) td_chunk_warp(d, sm, st, cur.cq[x], ctx, fs);
-    for (int32_t x = gw; x < c[1]; x += nw) td_vertex_warp(d, sm, st, cur.bin(1)[x], ctx, fs);
+    // one index space over the level's items (chunks of big rows, bin-1 rows, groups of
+    // 32 bin-0 rows), so that no warp takes an item of each kind while others idle
+    const int32_t gw = gwarp_spread(), nw = gridDim.x * WPB;
+    const int32_t c31 = c[3] + c[1], tot = c31 + (c[0] + 31) / 32;
     const int32_t *b0 = cur.bin(0);
-    for (int32_t x = gw * 32; x < c[0]; x += nw * 32) td_small_chunk(d, sm, st, b0, x, min(32, c[0] - x), ctx, fs);
+    for (int32_t x = gw; x < tot; x += nw) {
+      if (x < c[3]) td_chunk_warp(d, sm, st, cur.cq[x], ctx, fs);
+      else if (x < c31) td_vertex_warp(d, sm, st, cur.bin(1)[x - c[3]], ctx, fs);
+      else {
+        const int32_t x0 = (x - c31) * 32;
+        td_small_chunk(d, sm, st, b0, x0, min(32, c[0] - x0), ctx, fs);
+      }
+    }
   }
   bfs_flush(d, sm, st, ctx, fs);
   gsync(d, grid, sm);
@@ -1016,7 +1106,7 @@ __device__ __forceinline__ void bfs_expand_level(const Dev &d, cg::grid_group &g
       }
       {
         WarpG g{(int)(threadIdx.x & 31)};
-        const int32_t gw = blockIdx.x * WPB + (threadIdx.x >> 5), nw = gridDim.x * WPB;
+        const int32_t gw = gwarp_spread(), nw = gridDim.x * WPB;
         for (int32_t x = gw; x < q1; x += nw) bfs_bottom_up_b(d, g, sm, st, ctx, bul[x], fs);
       }
       bfs_flush(d, sm, st, ctx, fs);
@@ -1212,7 +1302,10 @@ __device__ __forceinline__ void discharge_chunk(const Dev &d, Smem &sm, long lon
   const int32_t n = d.n;
   const int32_t rbeg = d.row[u], rend = d.row[u + 1];
   const int32_t csz = dis_csize(d, rend - rbeg);
-  const int32_t beg = rbeg + (int32_t)(ce >> 32) * csz;
+  const uint32_t kraw = (uint32_t)(ce >> 32);
+  const bool probe = (kraw & PROBE_BIT) != 0;
+  const int32_t kc = (int32_t)(kraw & ~PROBE_BIT);
+  const int32_t beg = rbeg + kc * csz;
   const int32_t end = min(rend, beg + csz);
   const int32_t nch = (rend - rbeg + csz - 1) / csz;
   const unsigned long long t_start = d.trace ? gtimer() : 0;
@@ -1282,9 +1375,31 @@ __device__ __forceinline__ void discharge_chunk(const Dev &d, Smem &sm, long lon
     }
   }
   nmin = (uint32_t)g.min(dry ? 0ull : (unsigned long long)nmin);
-  if (g.any(pushes > 0)) __threadfence();   // every lane's pushes land before u can be taken again
+  const bool pushed = g.any(pushes > 0);
+  if (pushed) __threadfence();              // every lane's pushes land before u can be taken again
   __syncwarp();
+  if (probe) {                              // current-arc probe (async ring only)
+    if (lane == 0) {
+      if (pushed && ldv(d.arc + u) != kc) d.arc[u] = kc;
+      const long long eu = ldv(d.e + u) * k.sign;
+      if (eu > 0 && hu < n && hu <= glim) {
+        enqueue_items(d, u, tag, nch, 0u);  // excess left: every chunk (u stays queued; their last one releases it)
+      } else {
+        atomicExch(d.inq + u, 0);
+        __threadfence();
+        if (hu < n && hu > glim) sstat_add(sm, ST_GAP_SKIPS, 1);
+        else if (hu < n && ldv(d.e + u) * k.sign > 0) activate(d, k, nxt, u, tag, sm);
+        sstat_add(sm, ST_DIS_V, 1);
+      }
+      DBG(d, 205, u, (int32_t)kc, (int32_t)pushes, 0);
+      atomicAdd(&sm.work, scanned + 16ull);
+      sstat_add(sm, ST_DIS_SLOTS, scanned);
+    }
+    sstat_add(sm, ST_PUSHES, pushes);
+    return;
+  }
   if (lane == 0) {
+    if (pushes > 0 && d.arc && ldv(d.arc + u) != kc) d.arc[u] = kc;
     if (nmin < (uint32_t)DMIN_NONE) atomicMin(d.dmin + u, (int32_t)nmin);
     __threadfence();
     const int32_t done = atomicAdd(d.dcnt + u, 1);
@@ -1336,7 +1451,7 @@ __device__ __forceinline__ void process_dis(const BL &bl, const int32_t c[NB], i
     WarpG g{(int)(threadIdx.x & 31)};
     const int32_t nwi = c[3] + c[1];
     const int32_t nw = gridDim.x * WPB;
-    int32_t x = blockIdx.x * WPB + (threadIdx.x >> 5);
+    int32_t x = gwarp_spread();
     while (x < nwi) {
       if (x < c[3]) chunk(bl.cq[x]);
       else warp1(g, bl.bin(1)[x - c[3]]);
@@ -1348,7 +1463,7 @@ __device__ __forceinline__ void process_dis(const BL &bl, const int32_t c[NB], i
     TileG<8> g((int)(threadIdx.x & 31));
     const int32_t *b = bl.bin(0);
     const int32_t ntl = (gridDim.x * NT) >> 3;
-    int32_t x = (blockIdx.x * NT + threadIdx.x) >> 3;
+    int32_t x = (int32_t)((threadIdx.x >> 3) * gridDim.x + blockIdx.x);
     while (x < c[0]) {
       tile0(g, b[x]);
       if (g.rank() == 0) x = ntl + atomicAdd(cl + 2, 1);
@@ -1420,7 +1535,7 @@ __device__ __forceinline__ void rie(const Dev &d, const G &g, Smem &sm, int32_t 
 __device__ __forceinline__ void rie_chunks(const Dev &d, Smem &sm, const long long *cq, int32_t cnt, const BL &nxt,
                                            unsigned long long *workc) {
   const int lane = threadIdx.x & 31;
-  const int32_t gw = blockIdx.x * WPB + (threadIdx.x >> 5), nw = gridDim.x * WPB;
+  const int32_t gw = gwarp_spread(), nw = gridDim.x * WPB;
   WarpG g{lane};
   for (int32_t x = gw; x < cnt; x += nw) {
     const long long ce = cq[x];
@@ -1686,7 +1801,7 @@ __device__ int device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseCl
       // heights: 0 for roots, |V| for the rest of the track's region, |V|+1 outside it
       FS fs;
       long long mu0 = 0, mu1 = 0;
-      const BfsCtx c0{0, 0, false, 0u, 0u, BL{L.q0, qc, n, L.qc0},
+      const BfsCtx c0{0, 0, certify ? BCH : CH, false, 0u, 0u, BL{L.q0, qc, n, L.qc0},
                       BL{L.wl0, wlc, n, L.cw0}, ctl->fs};
       for (int32_t b = blockIdx.x * NT + (threadIdx.x & ~31); b < N; b += nt) {
         const int32_t x = b + (threadIdx.x & 31);
@@ -1775,7 +1890,8 @@ __device__ int device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseCl
       const bool bu1 = f1 > 0 && (unsigned long long)f1 * d.bu_alpha > (unsigned long long)(mu[1] > 0 ? mu[1] : 0);
       const bool dn0 = !bu0 && f0 > 0 && (unsigned long long)f0 * d.dense_div >= (unsigned long long)d.S;
       const bool dn1 = !bu1 && f1 > 0 && (unsigned long long)f1 * d.dense_div >= (unsigned long long)d.S;
-      const BfsCtx ctx{lvl, lvl + 1, collect, (bu0 ? 1u : 0u) | (bu1 ? 2u : 0u), (dn0 ? 1u : 0u) | (dn1 ? 2u : 0u),
+      const BfsCtx ctx{lvl, lvl + 1, certify ? BCH : CH, collect, (bu0 ? 1u : 0u) | (bu1 ? 2u : 0u),
+                       (dn0 ? 1u : 0u) | (dn1 ? 2u : 0u),
                        BL{L.q((lvl + 1) & 1), qc + NB * ((lvl + 1) % 3), n, L.qc((lvl + 1) & 1)},
                        BL{L.wl0, wlc, n, L.cw0}, ctl->fs + 2 * ((lvl + 1) % 3)};
       if (lead && (bu0 || bu1)) sstat_add(sm, ST_BU_LEVELS, 1);
@@ -1789,7 +1905,7 @@ __device__ int device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseCl
             if (dn0 && ldv(d.hp + v) == lvl + 1) { tr = 0; front = true; }
             else if (dn1 && ldv(d.hm + v) == lvl + 1) { tr = 1; front = true; }
             if (front) act = activity(d, collect, tr, v);
-          }, g0, g1, v0, v1);
+          }, g0, g1, v0, v1, ctx.bch);
         BlockG bg{sm.red};
         g0 = bg.sum(g0); g1 = bg.sum(g1);
         const long long nv0 = bg.sum(v0), nv1 = bg.sum(v1);
@@ -1880,7 +1996,7 @@ __device__ int device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseCl
         gsync(d, grid, sm);
         {
           const int32_t nc = cta_ld(sm, ctl->tcq + NB * cur + 3);
-          const int32_t gw = blockIdx.x * WPB + (threadIdx.x >> 5), nw = gridDim.x * WPB;
+          const int32_t gw = gwarp_spread(), nw = gridDim.x * WPB;
           for (int32_t x = gw; x < nc; x += nw) discharge_chunk(d, sm, tch.cq[x], rl, tch);
           dis_flush(d, sm, tch, rl);
         }
@@ -2063,41 +2179,81 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(const __grid_con
     auto eadd = [&](int32_t x, long long delta) {
       if (x == d.s) ds += delta; else if (x == d.t) dt += delta; else atom_add(d.e + x, delta);
     };
-    for (int64_t j = gt; j < d.k; j += nt) {
-      const int32_t u = d.bu[j], v = d.bv[j], c = d.bc[j];
-      int32_t i = -1;
-      if (u < 0 || u >= n || v < 0 || v >= n) set_status(d, -1, (int32_t)j);
-      else if (c < 0 || c > 1073741823) set_status(d, -7, (int32_t)j);
-      else if ((i = find_slot(d, u, v)) < 0) set_status(d, -2, (int32_t)j);
-      else if (atomicExch(d.stamp + i, d.batch_id) == d.batch_id) set_status(d, -3, (int32_t)j);
-      d.bslot[j] = i;
-      if (i < 0) continue;
-      const int32_t ri = d.rev[i];
-      const int32_t delta = c - ldv(d.cap + i);
-      atomicAdd(d.cap + i, delta);
-      int32_t r = atomicAdd(d.res + i, delta) + delta;
-      atomicAdd(d.rres + ri, delta);
-      int32_t dd = 0, sat = 0;
-      if (r < 0) {                                 // flow on (u,v) above the new capacity
-        dd = -r;
-        atomicAdd(d.res + i, dd);
-        atomicAdd(d.rres + ri, dd);
-        atomicAdd(d.res + ri, -dd);
-        atomicAdd(d.rres + i, -dd);
-        eadd(u, (long long)dd);
-        eadd(v, -(long long)dd);
-        r = 0;
+    // Two entries per thread per step, every independent load of both issued before the
+    // first dependent use (the pass is bound by dependent random accesses).
+    constexpr int EU = 2;
+    for (int64_t j0 = gt; j0 < d.k; j0 += (int64_t)EU * nt) {
+      int32_t u[EU], v[EU], c[EU], lo[EU], hi[EU], i[EU], st[EU], ri[EU], cap0[EU];
+      uint8_t pu[EU], pv[EU];
+      bool ok[EU];
+      int2 e0[EU];
+      uint32_t h0[EU];
+#pragma unroll
+      for (int q = 0; q < EU; q++) {               // entry, row bounds, parts, first probe
+        const int64_t j = j0 + (int64_t)q * nt;
+        ok[q] = j < d.k;
+        u[q] = ok[q] ? d.bu[j] : 0; v[q] = ok[q] ? d.bv[j] : 0; c[q] = ok[q] ? d.bc[j] : 0;
+        if (ok[q] && (u[q] < 0 || u[q] >= n || v[q] < 0 || v[q] >= n)) { set_status(d, -1, (int32_t)j); ok[q] = false; }
+        else if (ok[q] && (c[q] < 0 || c[q] > 1073741823)) { set_status(d, -7, (int32_t)j); ok[q] = false; }
+        lo[q] = ok[q] ? d.row[u[q]] : 0; hi[q] = ok[q] ? d.row[u[q] + 1] : 0;
+        pu[q] = (ok[q] && mode == MODE_PP) ? ldv(d.part + u[q]) : (uint8_t)0;
+        pv[q] = (ok[q] && mode == MODE_PP) ? ldv(d.part + v[q]) : (uint8_t)0;
+        h0[q] = ok[q] ? slot_hash(u[q], v[q]) & (uint32_t)d.hmask : 0u;
+        e0[q] = ok[q] ? __ldg(d.htab + h0[q]) : make_int2(-1, -1);
       }
-      if (mode == MODE_PP && r > 0 && ldv(d.part + u) == PART_S && ldv(d.part + v) == PART_T) {
-        sat = r;                                   // saturate the touched S->T slot
-        atomicAdd(d.res + i, -r);
-        atomicAdd(d.rres + ri, -r);
-        atomicAdd(d.res + ri, r);
-        atomicAdd(d.rres + i, r);
-        eadd(v, (long long)r);
-        eadd(u, -(long long)r);
+#pragma unroll
+      for (int q = 0; q < EU; q++) {               // resolve the slot (rarely a second probe)
+        i[q] = -1;
+        if (!ok[q]) continue;
+        if (e0[q].x == v[q] && e0[q].y >= lo[q] && e0[q].y < hi[q]) i[q] = e0[q].y;
+        else if (e0[q].x >= 0) {
+          for (uint32_t h = (h0[q] + 1) & (uint32_t)d.hmask;; h = (h + 1) & (uint32_t)d.hmask) {
+            const int2 e = __ldg(d.htab + h);
+            if (e.x == v[q] && e.y >= lo[q] && e.y < hi[q]) { i[q] = e.y; break; }
+            if (e.x < 0) break;
+          }
+        }
+        if (i[q] < 0) { set_status(d, -2, (int32_t)(j0 + (int64_t)q * nt)); ok[q] = false; }
       }
-      d.brec[3 * j] = delta; d.brec[3 * j + 1] = dd; d.brec[3 * j + 2] = sat;
+#pragma unroll
+      for (int q = 0; q < EU; q++) {               // duplicate stamp, capacity, reverse slot
+        const int64_t j = j0 + (int64_t)q * nt;
+        if (j < d.k) d.bslot[j] = ok[q] ? i[q] : -1;
+        st[q] = ok[q] ? atomicExch(d.stamp + i[q], d.batch_id) : 0;
+        cap0[q] = ok[q] ? ldv(d.cap + i[q]) : 0;
+        ri[q] = ok[q] ? d.rev[i[q]] : 0;
+      }
+#pragma unroll
+      for (int q = 0; q < EU; q++) {
+        if (!ok[q]) continue;
+        const int64_t j = j0 + (int64_t)q * nt;
+        const int32_t delta = c[q] - cap0[q];
+        atomicAdd(d.cap + i[q], delta);
+        int32_t r = atomicAdd(d.res + i[q], delta) + delta;
+        atomicAdd(d.rres + ri[q], delta);
+        int32_t dd = 0, sat = 0;
+        if (r < 0) {                               // flow on (u,v) above the new capacity
+          dd = -r;
+          atomicAdd(d.res + i[q], dd);
+          atomicAdd(d.rres + ri[q], dd);
+          atomicAdd(d.res + ri[q], -dd);
+          atomicAdd(d.rres + i[q], -dd);
+          eadd(u[q], (long long)dd);
+          eadd(v[q], -(long long)dd);
+          r = 0;
+        }
+        if (mode == MODE_PP && r > 0 && pu[q] == PART_S && pv[q] == PART_T) {
+          sat = r;                                 // saturate the touched S->T slot
+          atomicAdd(d.res + i[q], -r);
+          atomicAdd(d.rres + ri[q], -r);
+          atomicAdd(d.res + ri[q], r);
+          atomicAdd(d.rres + i[q], r);
+          eadd(v[q], (long long)r);
+          eadd(u[q], -(long long)r);
+        }
+        d.brec[3 * j] = delta; d.brec[3 * j + 1] = dd; d.brec[3 * j + 2] = sat;
+        if (st[q] == d.batch_id) set_status(d, -3, (int32_t)j);   // a second entry for this slot
+      }
     }
     auto flush_st = [&]() {
       const long long a = bg.sum(ds), b = bg.sum(dt);
@@ -2136,21 +2292,42 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(const __grid_con
       // new roots (T-deficits for h+, S-excess for h-, Alg.8 l.16-24) drop to 0 and
       // the active ones seed round 0's worklist (ring slot 0, deduplicated by inq)
       const BL wl0{d.wl, ctl->wlc, n, d.cw0};
-      for (int64_t j = gt; j < 2 * d.k; j += nt) {
-        const int32_t x = (j & 1) ? d.bv[j >> 1] : d.bu[j >> 1];
-        if (x == d.s || x == d.t) continue;
-        const uint8_t p = ldv(d.part + x);
-        const long long ev = ldv(d.e + x);
-        if (p == PART_T) {
-          if (ev < 0) {
-            const int32_t old = atomicExch(d.hp + x, 0);          // (x may be named by several entries)
-            if (old != 0 && old < n) gap_move(d, sm, 0, old, 0);
-          } else if (ev > 0 && ldv(d.hp + x) < n) activate(d, make_track(d, 0), wl0, x, 0u, sm, false);
-        } else if (p == PART_S) {
-          if (ev > 0) {
-            const int32_t old = atomicExch(d.hm + x, 0);
-            if (old != 0 && old < n) gap_move(d, sm, 1, old, 0);
-          } else if (ev < 0 && ldv(d.hm + x) < n) activate(d, make_track(d, 1), wl0, x, TRACK_BIT, sm, false);
+      constexpr int EW = 4;                        // endpoints per thread per step (loads first)
+      for (int64_t j0 = gt; j0 < 2 * d.k; j0 += (int64_t)EW * nt) {
+        int32_t x[EW], hx[EW];
+        uint8_t p[EW];
+        long long ev[EW];
+#pragma unroll
+        for (int q = 0; q < EW; q++) {
+          const int64_t j = j0 + (int64_t)q * nt;
+          x[q] = j < 2 * d.k ? ((j & 1) ? d.bv[j >> 1] : d.bu[j >> 1]) : d.s;
+        }
+#pragma unroll
+        for (int q = 0; q < EW; q++) {
+          const bool live = x[q] != d.s && x[q] != d.t;
+          p[q] = live ? ldv(d.part + x[q]) : (uint8_t)PART_NONE;
+          ev[q] = live ? ldv(d.e + x[q]) : 0;
+        }
+#pragma unroll
+        for (int q = 0; q < EW; q++)
+          hx[q] = p[q] == PART_T ? ldv(d.hp + x[q]) : (p[q] == PART_S ? ldv(d.hm + x[q]) : 0);
+#pragma unroll
+        for (int q = 0; q < EW; q++) {
+          if (p[q] == PART_T) {
+            if (ev[q] < 0) {
+              if (hx[q] != 0) {
+                const int32_t old = atomicExch(d.hp + x[q], 0);      // (x may be named by several entries)
+                if (old != 0 && old < n) gap_move(d, sm, 0, old, 0);
+              }
+            } else if (ev[q] > 0 && hx[q] < n) activate(d, make_track(d, 0), wl0, x[q], 0u, sm, false);
+          } else if (p[q] == PART_S) {
+            if (ev[q] > 0) {
+              if (hx[q] != 0) {
+                const int32_t old = atomicExch(d.hm + x[q], 0);
+                if (old != 0 && old < n) gap_move(d, sm, 1, old, 0);
+              }
+            } else if (ev[q] < 0 && hx[q] < n) activate(d, make_track(d, 1), wl0, x[q], TRACK_BIT, sm, false);
+          }
         }
       }
       {

@@ -86,3 +86,74 @@ for lo in edges:
     fl = ((items[:, 0] < hi) & (items[:, 1] > lo)).sum()
     stt = ((items[:, 0] >= lo) & (items[:, 0] < hi)).sum()
     print(f"  t={lo:6.0f}-{hi:<6.0f} in-flight {fl:5d} started {stt:5d}")
+
+# ---- critical path: each item's predecessor = the item whose warp enqueued its vertex
+# (the latest enqueue of that vertex before the item's claim)
+enq_rows = R[R[:, 0] == 202]
+enq_t = ts[R[:, 0] == 202]
+claim_rows = R[R[:, 0] == 203]
+claim_t = ts[R[:, 0] == 203]
+# item intervals per warp, to map (warp, time) -> item index
+order = np.lexsort((items[:, 0], ))
+by_warp = {}
+item_warp = []
+for idx, (a, b, v, k, x) in enumerate(items):
+    pass
+# rebuild items with warp ids
+items2 = []
+for w in np.unique(R[:, 2]):
+    m = R[:, 2] == w
+    rw, tw = R[m], ts[m]
+    o = np.argsort(tw, kind="stable"); rw, tw = rw[o], tw[o]
+    st_ = None
+    for r, tt in zip(rw, tw):
+        if r[0] in (200, 204): st_ = (tt, r)
+        elif r[0] in (201, 205) and st_ is not None:
+            items2.append((st_[0], tt, int(st_[1][1]), int(st_[1][0]), int(w)))
+            st_ = None
+items2.sort()
+I = np.array(items2, dtype=np.float64)
+from collections import defaultdict
+warp_items = defaultdict(list)
+for idx, it in enumerate(items2):
+    warp_items[it[4]].append((it[0], it[1], idx))
+def item_at(w, t):
+    for a, b, idx in warp_items.get(w, []):
+        if a - 0.01 <= t <= b + 0.01:
+            return idx
+    return -1
+# enqueues of vertex v: (time, producing item)
+enq_by_v = defaultdict(list)
+for r, tt in zip(enq_rows, enq_t):
+    enq_by_v[int(r[1])].append((tt, item_at(int(r[2]), tt)))
+pred = np.full(len(items2), -1)
+for idx, (a, b, v, kind, w) in enumerate(items2):
+    lst = [x for x in enq_by_v.get(v, []) if x[0] <= a]
+    if lst:
+        pred[idx] = lst[-1][1]
+# longest chain ending at each item by end time
+dist = np.zeros(len(items2))
+for idx in range(len(items2)):
+    p = pred[idx]
+    dist[idx] = (items2[idx][1] - items2[idx][0]) + (dist[p] if p >= 0 else 0)
+# the stage-1 phase: items before the first idle gap of >= 20 us
+srt = np.argsort(I[:, 0])
+cut_t = I[:, 1].max()
+run_end = I[srt[0], 1]
+for ii in srt:
+    if I[ii, 0] > run_end + 20:
+        cut_t = run_end; break
+    run_end = max(run_end, I[ii, 1])
+sel = np.nonzero(I[:, 1] <= cut_t + 0.01)[0]
+end = int(sel[np.argmax(I[sel, 1])])
+print(f"phase ends at {I[end, 1]:.1f} us ({len(sel)} items); last item's chain busy time {dist[end]:.1f} us; "
+      f"max chain busy {dist[sel].max():.1f} us")
+chain = []
+c = end
+while c >= 0 and len(chain) < 200:
+    chain.append(c); c = pred[c]
+chain = chain[::-1]
+print(f"critical chain: {len(chain)} items")
+for c in chain[-60:]:
+    a, b, v, kind, w = items2[c]
+    print(f"   t={a:7.1f}-{b:7.1f} ({b-a:5.1f} us) {'chunk' if kind == 204 else 'vertex'} v={v} deg={deg[v]} part={lab['part'][v]} hp={lab['hp'][v]} hm={lab['hm'][v]}")

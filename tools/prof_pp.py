@@ -1,17 +1,19 @@
-"""Launch sequence for ncu: static solve (launch 1), PP batch (2), PP batch (3, profiled), cut (4)."""
+"""Launch sequence for ncu, the bench's protocol: static solve (launch 0), then DYN_PP
+batches each followed by the S_min query: pp0 (1), cut0 (2), pp1 (3), cut1 (4), pp2 (5) ...
+usage: python tools/prof_pp.py [scale] [nbatches] [algo]"""
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import workloads as W
 import paper_2511_05895_b200 as P
 
-algo = sys.argv[1] if len(sys.argv) > 1 else "pp"
-g = W.rmat(20, 16, 1, 7)
+scale = int(sys.argv[1]) if len(sys.argv) > 1 else 20
+nb = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+algo = sys.argv[3] if len(sys.argv) > 3 else "pp"
+g, batches = W.sequence(dict(kind="rmat", scale=scale, frac=0.01, nb=nb))
 f = P.DynMaxFlow.from_graph(g)
 f.static_solve()
-cs = W.CapState(g)
-for j in range(2):
-    b = W.rmat_batch(g, cs, 0.01, 100 + j)
-    cs.apply(b)
+for b in batches:
     f.apply_batch(b.u, b.v, b.new_cap, algo=algo)
-f.min_cut_source_side()
-print("done", f.flow_value(), f.stats()["device_ms"])
+    print("batch ms", f.stats()["device_ms"], flush=True)
+    f.min_cut_source_side()
+print("done", f.flow_value())

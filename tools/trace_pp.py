@@ -20,10 +20,14 @@ def show(tag):
     for ri, r in enumerate(f.trace()):
         ex = r['extra']
         extra = f"bu={ex & 3} ch={ex >> 3}" if r['phase'] == 'bfs' else f"x={ex}"
+        if r['phase'] == 'bfs' and r['slow_us'] > 0:
+            extra += f" slowchunk={r['slow_us']:.1f}us v={(int(r['slow_deg']) << 8) | int(r['slow_cyc'])}"
         if r['phase'] == 'discharge':
             extra += f" slow={r['slow_us']:.1f}us deg={r['slow_deg']} cyc={r['slow_cyc']}"
         c = np.sort(cta[ri]) if ri < len(cta) else np.zeros(1)
         dist = f"cta busy p50={c[len(c) // 2]:.1f} p90={c[int(len(c) * .9)]:.1f} max={c[-1]:.1f}"
+        if ri < len(cta) and len(cta[ri]):
+            dist += f" (cta {int(np.argmax(cta[ri]))})"
         print(f"  {r['phase']:9s} it={r['iter']:<3d} sub={r['sub']:<4d} items={r['items']:<9d} {extra:16s} {r['us']:9.1f} us  {dist}")
 f.static_solve_pp(); show("static_pp")
 f.static_solve(); show("static")
@@ -36,3 +40,4 @@ for j in range(skip + nshow):
 m = f.min_cut_source_side(); show("mincut (cached)")
 b = W.rmat_batch(g, cs, 0.01, 100 + skip + nshow); cs.apply(b)
 f.apply_batch(b.u, b.v, b.new_cap, algo="pr"); show("pr")
+m = f.max_cut_source_side(); show("maxcut")
