@@ -1649,7 +1649,7 @@ __device__ __forceinline__ void async_phase(const Dev &d, Smem &sm, const BL &in
         stop = true;
         sstat_add(sm, ST_TAIL_STOPS, 1);
       }
-      if (!stop && sm.work > 32768ull) {                                  // budget: flushed in 32K-slot units
+      if (!stop && *(volatile unsigned long long *)&sm.work > 32768ull) {  // budget: flushed in 32K-slot units
         const unsigned long long w = atomicExch(&sm.work, 0ull);
         stop = (long long)(atomicAdd(&ctl->awork, w) + w) > d.work_budget;
       }
@@ -2000,7 +2000,8 @@ __device__ int device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseCl
           for (int32_t x = gw; x < nc; x += nw) discharge_chunk(d, sm, tch.cq[x], rl, tch);
           dis_flush(d, sm, tch, rl);
         }
-        if (threadIdx.x == 0 && sm.work) { atomicAdd(ctl->work + cur, sm.work); sm.work = 0; }
+        __syncthreads();                          // every warp's work is in sm.work
+        if (threadIdx.x == 0) { const unsigned long long w_ = atomicExch(&sm.work, 0ull); if (w_) atomicAdd(ctl->work + cur, w_); }
         if (lead) { sstat_add(sm, ST_ROUNDS, 1); sstat_add(sm, ST_TOPO_ROUNDS, 1); }
         gsync(d, grid, sm);
         clk.lap(d, sm, ST_T_DIS, iter, r, ndom, 0);
@@ -2023,7 +2024,8 @@ __device__ int device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseCl
       const BL init{L.wl0, wlc, n, L.cw0};
       async_phase(d, sm, init, w, rl, BL{L.wl1, wlc + NB, n, L.cw1});
       dis_flush(d, sm, BL{L.wl1, wlc + NB, n, L.cw1}, rl);
-      if (threadIdx.x == 0 && sm.work) { atomicAdd(&ctl->awork, sm.work); sm.work = 0; }
+      __syncthreads();
+      if (threadIdx.x == 0) { const unsigned long long w_ = atomicExch(&sm.work, 0ull); if (w_) atomicAdd(&ctl->awork, w_); }
       if (lead) sstat_add(sm, ST_ROUNDS, 1);
       gsync(d, grid, sm);
       clk.lap(d, sm, ST_T_DIS, iter, 0, total(w), w[3]);
@@ -2048,7 +2050,8 @@ __device__ int device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseCl
                   [&](const WarpG &g, int32_t entry) { discharge(d, g, sm, entry, rl, nxt, ctl->work + cur); },
                   [&](const TileG<8> &g, int32_t entry) { discharge(d, g, sm, entry, rl, nxt, ctl->work + cur); });
       dis_flush(d, sm, nxt, rl);
-      if (threadIdx.x == 0 && sm.work) { atomicAdd(ctl->work + cur, sm.work); sm.work = 0; }
+      __syncthreads();
+      if (threadIdx.x == 0) { const unsigned long long w_ = atomicExch(&sm.work, 0ull); if (w_) atomicAdd(ctl->work + cur, w_); }
       if (lead) sstat_add(sm, ST_ROUNDS, 1);
       gsync(d, grid, sm);
       clk.lap(d, sm, ST_T_DIS, iter, r, total(w), w[3]);
