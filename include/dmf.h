@@ -65,7 +65,7 @@ typedef enum {
 /* Discharge schedules (dmf_options.schedule).  Every schedule computes the same F,
  * S_min and S_max; they differ only in how active vertices are found and ordered. */
 typedef enum {
-    DMF_SCHED_AUTO = 0,      /* repairs: ASYNC; static solve: ROUNDS with the topology auto-switch */
+    DMF_SCHED_AUTO = 0,      /* repairs: ASYNC; static solve: ROUNDS (topology auto-switch: topo_div) */
     DMF_SCHED_ASYNC = 1,     /* data-driven worklist seeding a device-wide ring queue: a vertex
                                 made active by a push is processed at once (the property P:647 credits
                                 to the topology-driven schedule) */
@@ -101,8 +101,9 @@ typedef struct {
                                counts): 0 => on, < 0 => off [DMF_LOCAL_GAP] */
     int32_t warm;           /* DYN_PP after DYN_PP starts from the previous call's labels: 0 => on,
                                < 0 => off (every repair starts with a fresh global relabel) [DMF_WARM] */
-    int32_t topo_div;       /* ROUNDS/AUTO: a round runs topology-driven when more than n / topo_div
-                               vertices are active; 0 => 16, < 0 => never [DMF_TOPO_DIV] */
+    int32_t topo_div;       /* auto-switch: a discharge phase runs topology-driven when more than
+                               n / topo_div vertices are active; <= 0 => never (default: the worklist
+                               won every A/B on B200) [DMF_TOPO_DIV] */
     int32_t check_level;    /* 0 => off; 1 => after every solve / repair the device checks the cheap
                                invariants (0 <= res <= cap + cap_rev, res[i] + res[rev[i]] = cap[i] +
                                cap[rev[i]], mirror consistency, sum of e = 0) and the call fails with

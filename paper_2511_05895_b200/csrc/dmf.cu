@@ -77,7 +77,7 @@ struct dmf_graph {
   int32_t async_sleep_ns = 128;
   int32_t tail_items = 2048;
   int32_t local_gap = 1;
-  int32_t topo_div = 16;
+  int32_t topo_div = 0;
   int32_t check_level = 0;
   int32_t lazy = 1;          // DYN_PP warm start certified by the universal backward BFS
   int32_t dmaxch = 0;
@@ -623,7 +623,9 @@ int dmf_create(int32_t n, const int64_t *row_ptr, const int32_t *col, const int3
     g->no_warm = knob(o.warm, "DMF_WARM") < 0;
     if (const char *nw = getenv("DMF_NO_WARM")) g->no_warm = atoi(nw) != 0;
     const int32_t td = knob(o.topo_div, "DMF_TOPO_DIV");
-    g->topo_div = sched == DMF_SCHED_TOPOLOGY ? 0x3fffffff : (td == 0 ? 16 : (td < 0 ? 0 : td));
+    // the auto-switch is off by default: on B200 the worklist (its compaction fused into
+    // the BFS) beat every topology-driven variant measured (tools/ab_topology.py)
+    g->topo_div = sched == DMF_SCHED_TOPOLOGY ? 0x3fffffff : (td <= 0 ? 0 : td);
     g->lazy = knob(o.certify, "DMF_CERTIFY") < 0 ? 0 : 1;
     if (const char *mc = getenv("DMF_DMAXCH")) g->dmaxch = atoi(mc) > 0 ? atoi(mc) : 0;
     if (const char *pb = getenv("DMF_PROBE")) g->probes = atoi(pb) != 0;

@@ -1578,12 +1578,14 @@ constexpr uint32_t TAIL_PEND = 64;       // async: "tail" = at most this many it
 __device__ __forceinline__ long long ldvol(const long long *p) { return *(const volatile long long *)p; }
 __device__ __forceinline__ int32_t ldvol(const int32_t *p) { return *(const volatile int32_t *)p; }
 
+// (the CTA's cached stop flag and poll time are shared by its consumer warps: read and
+// written with shared-memory atomics)
 __device__ __forceinline__ bool async_stopped(const Dev &d, Smem &sm) {
-  if (sm.astop) return true;
+  if (atomicAdd(&sm.astop, 0)) return true;
   const unsigned long long now = gtimer();
-  if (now - sm.apoll > 1000) {             // one global poll per CTA per microsecond
-    sm.apoll = now;
-    if (ldvol(&d.ctl->astop)) { sm.astop = 1; return true; }
+  if (now - atomicAdd(&sm.apoll, 0ull) > 1000) {   // one global poll per CTA per microsecond
+    atomicExch(&sm.apoll, now);
+    if (ldvol(&d.ctl->astop)) { atomicExch(&sm.astop, 1); return true; }
   }
   return false;
 }
@@ -1653,7 +1655,7 @@ __device__ __forceinline__ void async_phase(const Dev &d, Smem &sm, const BL &in
         const unsigned long long w = atomicExch(&sm.work, 0ull);
         stop = (long long)(atomicAdd(&ctl->awork, w) + w) > d.work_budget;
       }
-      if (stop) { if (!ldvol(&ctl->astop)) atomicExch(&ctl->astop, 1); sm.astop = 1; }
+      if (stop) { if (!ldvol(&ctl->astop)) atomicExch(&ctl->astop, 1); atomicExch(&sm.astop, 1); }
     }
   }
 }

@@ -61,6 +61,7 @@ KNOB_SETS = {
     "rounds": dict(schedule="rounds"),
     "topology": dict(schedule="topology"),
     "auto_topo_switch": dict(schedule="auto", topo_div=1000000),     # any active vertex -> topology phase
+    "auto_topo_n16": dict(topo_div=16),
     "no_gap": dict(local_gap=-1),
     "no_warm": dict(warm=-1),
     "no_certify": dict(certify=-1),
