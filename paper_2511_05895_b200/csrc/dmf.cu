@@ -81,6 +81,7 @@ struct dmf_graph {
   int32_t check_level = 0;
   int32_t lazy = 1;          // DYN_PP warm start certified by the universal backward BFS
   int32_t dmaxch = 0;
+  int32_t scan2 = 1;         // DMF_SCAN2=0: chunk discharge claims and pushes per 128-slot step
   int32_t imm_act = 1;       // DMF_IMM_ACT=0: stage pushed heads and check them after the item        // DMF_DMAXCH: chunk items per big-vertex discharge activation (0: CH slots each)
   long long budget_mul = 1;
   int32_t *cnt = nullptr, *cnt_next = nullptr;   // local-gap level counts (this call / next warm call)
@@ -305,6 +306,7 @@ static Dev make_dev(dmf_graph *g) {
   d.lazy = g->lazy;
   d.dmaxch = g->dmaxch;
   d.imm_act = g->imm_act;
+  d.scan2 = g->scan2;
   d.plist = g->plist; d.stamp = g->stamp;
   d.htab = g->htab; d.hmask = g->hmask;
   d.mask = g->mask; d.ctl = g->ctl;
@@ -630,6 +632,7 @@ int dmf_create(int32_t n, const int64_t *row_ptr, const int32_t *col, const int3
     if (const char *mc = getenv("DMF_DMAXCH")) g->dmaxch = atoi(mc) > 0 ? atoi(mc) : 0;
     if (const char *pb = getenv("DMF_PROBE")) g->probes = atoi(pb) != 0;
     if (const char *ia = getenv("DMF_IMM_ACT")) g->imm_act = atoi(ia) != 0;
+    if (const char *s2 = getenv("DMF_SCAN2")) g->scan2 = atoi(s2) != 0;
     g->check_level = knob(o.check_level, "DMF_CHECK_LEVEL");
     if (const char *ba = getenv("DMF_BU_ALPHA")) g->bu_alpha = atoi(ba) > 0 ? atoi(ba) : g->bu_alpha;
     if (const char *dd = getenv("DMF_DENSE_DIV")) g->dense_div = atoi(dd) > 0 ? atoi(dd) : g->dense_div;

@@ -137,6 +137,7 @@ struct Dev {
   int32_t check_level;
   int32_t imm_act;           // async discharge: activate a pushed head at the push (returning atomic) instead of after the item
   int32_t dmaxch;            // discharge: at most this many chunk items per big-vertex activation (0: CH-slot chunks)
+  int32_t scan2;             // chunked discharge: two-pass scan (list admissible slots, one claim, push)
   int32_t lazy;              // DYN_PP warm start: certify with the universal backward BFS (no pull BFS / stage 2)
   int32_t *plist;            // region P of push-pull stage 2
   int32_t *stamp;            // per-slot batch stamp (duplicate detection)

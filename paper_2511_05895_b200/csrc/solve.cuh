@@ -54,6 +54,8 @@ struct TileSm {
   int32_t base[8];
 };
 
+constexpr int32_t ADMCAP = 64;      // admissible slots listed per warp by a chunk scan (discharge_chunk)
+
 struct Smem {
   long long red[WPB + 1];
   unsigned long long stat[ST_N];
@@ -72,6 +74,7 @@ struct Smem {
   int32_t tslot;                   // topology round r: activity flag ctl->tact[r % 3]
   int32_t lvcnt[2];                // BFS: vertices labelled by this CTA in the current level, per track
   int32_t cand[2048];
+  int32_t adm_i[WPB * ADMCAP], adm_v[WPB * ADMCAP], adm_r[WPB * ADMCAP];   // chunk scan: admissible slots per warp
   Stage st;                    // block-staged appends (BFS)
   TileSm ts;                   // tiled compaction (dense top-down BFS levels)
 };
@@ -1324,7 +1327,85 @@ __device__ __forceinline__ void discharge_chunk(const Dev &d, Smem &sm, long lon
     glim = (int32_t)g.bcast(glim);
     dry = g.bcast(e0) <= 0 || hu > glim;  // above an emptied level: no pushes, and no lift below
   }
-  if (hu < n && !dry) {
+  if (hu < n && !dry && d.scan2) {
+    // Two passes: (1) a read-only scan of the whole chunk, 8 slots per lane per step
+    // with every load of a step issued before the first use, that records the
+    // admissible slots (h(v) < h(u)) in a per-warp shared list and the lowest height
+    // among the residual non-admissible ones; (2) ONE claim of the listed residual
+    // from e(u) and the pushes from the list.  A chunk with nothing admissible (most
+    // chunks of a hub's row) costs the scan only.  The slots of u's row in this track
+    // are pushed only by u's discharger, so a residual can only grow between the
+    // passes and every take stays <= the residual it was read as.
+    int32_t *ai = sm.adm_i + (threadIdx.x >> 5) * ADMCAP;
+    int32_t *av = sm.adm_v + (threadIdx.x >> 5) * ADMCAP;
+    int32_t *ar = sm.adm_r + (threadIdx.x >> 5) * ADMCAP;
+    const unsigned lt = (1u << lane) - 1u;
+    int32_t nadm = 0;                      // warp-uniform: admissible slots found
+    long long lsum = 0;                    // this lane's listed admissible residual
+    bool complete = true;                  // every slot of the chunk was examined
+    long long e0 = 0;
+    if (lane == 0) e0 = ldv(d.e + u) * k.sign;
+    e0 = g.bcast(e0);
+    for (int32_t b0 = beg; b0 < end; b0 += 256) {
+      int32_t r[8], v[8], h[8];
+#pragma unroll
+      for (int j = 0; j < 8; j++) {
+        const int32_t i = b0 + lane + 32 * j;
+        r[j] = i < end ? ldv(k.F + i) : 0;
+        v[j] = i < end ? d.dst[i] : 0;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; j++) h[j] = r[j] > 0 ? ldv(k.hgt + v[j]) : 0;
+#pragma unroll
+      for (int j = 0; j < 8; j++) {
+        const bool adm = r[j] > 0 && h[j] < hu;
+        if (r[j] > 0 && !adm) nmin = (uint32_t)h[j] < nmin ? (uint32_t)h[j] : nmin;
+        const unsigned m = __ballot_sync(0xffffffffu, adm);
+        if (m) {
+          const int32_t pos = nadm + __popc(m & lt);
+          if (adm && pos < ADMCAP) { ai[pos] = b0 + lane + 32 * j; av[pos] = v[j]; ar[pos] = r[j]; lsum += r[j]; }
+          nadm += __popc(m);
+        }
+      }
+      scanned += 256;
+      if (nadm >= ADMCAP || (b0 + 256 < end && g.sum(lsum) >= e0)) {   // list full / excess covered
+        complete = b0 + 256 >= end;
+        break;
+      }
+    }
+    const long long tot = g.sum(lsum);
+    long long got = 0;
+    if (tot > 0) {                         // claim the listed residual from e(u)
+      if (lane == 0) {
+        const long long old = (long long)atomicAdd(reinterpret_cast<unsigned long long *>(d.e + u),
+                                                   (unsigned long long)(-tot * k.sign)) * k.sign;
+        got = old <= 0 ? 0 : (old < tot ? old : tot);
+        if (got < tot) atom_add(d.e + u, (tot - got) * k.sign);   // refund what e(u) did not cover
+      }
+      got = g.bcast(got);
+    }
+    __syncwarp();
+    const int32_t nl = nadm < ADMCAP ? nadm : ADMCAP;
+    long long before = 0;                  // listed residual of earlier list entries
+    for (int32_t x0 = 0; x0 < nl && before < got; x0 += 32) {
+      const int32_t x = x0 + lane;
+      const int32_t r = x < nl ? ar[x] : 0;
+      long long t32;
+      const long long pre = before + g.exscan(r, t32);
+      long long take = got - pre;
+      take = take < 0 ? 0 : (take > r ? r : take);
+      if (take > 0) {
+        const int32_t i = ai[x];
+        push_slot(d, k, nxt, i, d.rev[i], av[x], (int32_t)take, tag, sm);
+        pushes++;
+      }
+      before += t32;
+    }
+    __syncwarp();
+    // dry: u's excess is gone, an admissible slot may remain, or part of the chunk was
+    // not examined -- no lift decided by this chunk
+    if (got < tot || nadm > ADMCAP || !complete) dry = true;
+  } else if (hu < n && !dry) {
     for (int32_t b0 = beg; b0 < end; b0 += 128) {   // warp-uniform trip count (collectives inside)
       const int32_t i0 = b0 + lane;
       int32_t r[4], v[4], h[4], ri[4];
