@@ -909,18 +909,29 @@ __device__ __forceinline__ void compact_domain(const Dev &d, TileSm &ts, int32_t
     int8_t fc[TILE_ITEMS], wc[TILE_ITEMS];
     uint32_t tg[TILE_ITEMS];
     int32_t nchv[TILE_ITEMS];
+    // classification loads of every item first, then the degree loads, then the
+    // appends (each stage's loads in flight together)
+    int trj[TILE_ITEMS];
+    bool frj[TILE_ITEMS], acj[TILE_ITEMS];
+    int32_t dgj[TILE_ITEMS];
 #pragma unroll
     for (int j = 0; j < TILE_ITEMS; j++) {
       const int32_t x = t0 + j * NT + threadIdx.x;
-      int32_t v = -1;
-      int tr = 0;
-      bool front = false, act = false;
-      int32_t deg = 0;
+      vv[j] = -1; trj[j] = 0; frj[j] = false; acj[j] = false;
       if (x < N) {
-        v = dom ? dom[x] : x;
-        classify(v, tr, front, act);
-        if (front || act) deg = d.row[v + 1] - d.row[v];
+        vv[j] = dom ? dom[x] : x;
+        classify(vv[j], trj[j], frj[j], acj[j]);
       }
+    }
+#pragma unroll
+    for (int j = 0; j < TILE_ITEMS; j++)
+      dgj[j] = (frj[j] || acj[j]) ? d.row[vv[j] + 1] - d.row[vv[j]] : 0;
+#pragma unroll
+    for (int j = 0; j < TILE_ITEMS; j++) {
+      const int32_t v = vv[j];
+      const int tr = trj[j];
+      const bool front = frj[j], act = acj[j];
+      const int32_t deg = dgj[j];
       const int fb = front ? (deg <= BIN0_MAX ? 0 : (deg <= BIN1_MAX ? 1 : 2)) : -1;
       const int wb = (collect && act) ? (deg <= BIN0_MAX ? 0 : (deg <= BIN1_MAX ? 1 : 2)) : -1;
       if (wb >= 0) d.inq[v] = 1;
@@ -1886,52 +1897,68 @@ __device__ int device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseCl
       long long mu0 = 0, mu1 = 0;
       const BfsCtx c0{0, 0, certify ? BCH : CH, false, 0u, 0u, BL{L.q0, qc, n, L.qc0},
                       BL{L.wl0, wlc, n, L.cw0}, ctl->fs};
-      for (int32_t b = blockIdx.x * NT + (threadIdx.x & ~31); b < N; b += nt) {
-        const int32_t x = b + (threadIdx.x & 31);
-        bool r0 = false, r1 = false, in0 = false, in1 = false;
-        int32_t v = 0;
-        if (x < N) {
-          v = on_plist ? d.plist[x] : x;
-          const long long ev = ldv(d.e + v);
-          if (kind == RK_PUSH || kind == RK_MAXCUT) {
-            r0 = v == d.t || (v != d.s && ev < 0);
-            in0 = v != d.s;
-            d.hp[v] = r0 ? 0 : n;
-          } else if (kind == RK_PP) {
-            const uint8_t p = ldv(d.part + v);
-            in0 = p == PART_T && v != d.s;
-            in1 = p == PART_S && v != d.t;
-            r0 = in0 && (v == d.t || ev < 0);
-            r1 = in1 && (v == d.s || ev > 0);
-            d.hp[v] = r0 ? 0 : (in0 ? n : n + 1);
-            d.hm[v] = r1 ? 0 : (in1 ? n : n + 1);
-          } else if (kind == RK_STAGE2) {       // P only; outside P heights stay >= |V| or
-            r0 = ev < 0;                        // belong to T\P, which no P vertex reaches
-            in0 = true;
-            d.hp[v] = r0 ? 0 : n;
-          } else if (kind == RK_RETURN_S) {     // t is outside the region: its excess is F
-            r0 = v == d.s;
-            in0 = v != d.t;
-            d.hp[v] = r0 ? 0 : (in0 ? n : n + 1);
-          } else if (kind == RK_FILL_T) {       // s is outside the region
-            r1 = v == d.t;
-            in1 = v != d.s;
-            d.hm[v] = r1 ? 0 : (in1 ? n : n + 1);
-          } else if (kind == RK_MINCUT_P) {     // forward reach of the excess left in P
-            r1 = ev > 0;
-            in1 = true;
-            d.hm[v] = r1 ? 0 : n;
-          } else {  // RK_MINCUT
-            r1 = v == d.s || (v != d.t && ev > 0);
-            in1 = v != d.t;
-            d.hm[v] = r1 ? 0 : n;
-          }
-          if ((in0 && !r0) || (in1 && !r1)) {
-            const long long deg = d.row[v + 1] - d.row[v];
-            if (in0 && !r0) mu0 += deg; else mu1 += deg;
-          }
+      // RU vertices per thread per step, every load of the step issued before the first
+      // use (the sweep is bound by dependent round trips, not bytes)
+      constexpr int RU = 4;
+      for (int32_t t0 = blockIdx.x * NT * RU; t0 < N; t0 += nt * RU) {
+        int32_t v[RU], deg[RU];
+        long long ev[RU];
+        uint8_t p[RU];
+        bool ok[RU];
+#pragma unroll
+        for (int j = 0; j < RU; j++) {
+          const int32_t x = t0 + j * NT + threadIdx.x;
+          ok[j] = x < N;
+          v[j] = ok[j] ? (on_plist ? d.plist[x] : x) : 0;
         }
-        claim_push(d, sm.st, c0, r0 || r1, false, v, r1 ? 1 : 0, fs);
+#pragma unroll
+        for (int j = 0; j < RU; j++) {
+          ev[j] = ok[j] ? ldv(d.e + v[j]) : 0;
+          p[j] = (ok[j] && kind == RK_PP) ? ldv(d.part + v[j]) : (uint8_t)0;
+          deg[j] = ok[j] ? d.row[v[j] + 1] - d.row[v[j]] : 0;
+        }
+#pragma unroll
+        for (int j = 0; j < RU; j++) {
+          bool r0 = false, r1 = false, in0 = false, in1 = false;
+          if (ok[j]) {
+            const int32_t x = v[j];
+            if (kind == RK_PUSH || kind == RK_MAXCUT) {
+              r0 = x == d.t || (x != d.s && ev[j] < 0);
+              in0 = x != d.s;
+              d.hp[x] = r0 ? 0 : n;
+            } else if (kind == RK_PP) {
+              in0 = p[j] == PART_T && x != d.s;
+              in1 = p[j] == PART_S && x != d.t;
+              r0 = in0 && (x == d.t || ev[j] < 0);
+              r1 = in1 && (x == d.s || ev[j] > 0);
+              d.hp[x] = r0 ? 0 : (in0 ? n : n + 1);
+              d.hm[x] = r1 ? 0 : (in1 ? n : n + 1);
+            } else if (kind == RK_STAGE2) {       // P only; outside P heights stay >= |V| or
+              r0 = ev[j] < 0;                     // belong to T\P, which no P vertex reaches
+              in0 = true;
+              d.hp[x] = r0 ? 0 : n;
+            } else if (kind == RK_RETURN_S) {     // t is outside the region: its excess is F
+              r0 = x == d.s;
+              in0 = x != d.t;
+              d.hp[x] = r0 ? 0 : (in0 ? n : n + 1);
+            } else if (kind == RK_FILL_T) {       // s is outside the region
+              r1 = x == d.t;
+              in1 = x != d.s;
+              d.hm[x] = r1 ? 0 : (in1 ? n : n + 1);
+            } else if (kind == RK_MINCUT_P) {     // forward reach of the excess left in P
+              r1 = ev[j] > 0;
+              in1 = true;
+              d.hm[x] = r1 ? 0 : n;
+            } else {  // RK_MINCUT
+              r1 = x == d.s || (x != d.t && ev[j] > 0);
+              in1 = x != d.t;
+              d.hm[x] = r1 ? 0 : n;
+            }
+            if (in0 && !r0) mu0 += deg[j];
+            else if (in1 && !r1) mu1 += deg[j];
+          }
+          claim_push_deg(d, sm.st, c0, r0 || r1, false, v[j], r1 ? 1 : 0, fs, deg[j]);
+        }
       }
       bfs_flush(d, sm, sm.st, c0, fs);
       BlockG bg{sm.red};
@@ -2218,6 +2245,38 @@ __device__ __forceinline__ long long saturate_slot(const Dev &d, int32_t i) {
   return r;
 }
 
+// Grid-stride sweep over the vertices [0, n), RU per thread per step: load(v) of all RU
+// vertices first (independent loads in flight together), then apply(v, x, ok) for each,
+// called by every lane (ok = v < n) so that apply may use warp collectives.
+template <class T, int RU = 4, class Load, class Apply>
+__device__ __forceinline__ void vsweep(int32_t n, Load load, Apply apply) {
+  const int32_t nt = gridDim.x * NT;
+  for (int32_t t0 = blockIdx.x * NT * RU; t0 < n; t0 += nt * RU) {
+    T x[RU];
+#pragma unroll
+    for (int j = 0; j < RU; j++) {
+      const int32_t v = t0 + j * NT + threadIdx.x;
+      x[j] = v < n ? load(v) : T{};
+    }
+#pragma unroll
+    for (int j = 0; j < RU; j++) {
+      const int32_t v = t0 + j * NT + threadIdx.x;
+      apply(v, x[j], v < n);
+    }
+  }
+}
+
+// warp-convergent histogram increment: lanes with the same bin add once (heights of a
+// BFS labelling take a handful of values, so per-lane shared atomics would serialise)
+__device__ __forceinline__ void hist_add(int32_t *hist, bool pred, int32_t idx) {
+  const unsigned act = __ballot_sync(0xffffffffu, pred);
+  if (!pred) return;
+  const unsigned grp = __match_any_sync(act, idx);
+  if ((int)(threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(hist + idx, __popc(grp));
+}
+
+struct VX { long long e; int32_t hp, hm; };
+
 template <int NTHREADS>
 __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(const __grid_constant__ Dev d, int32_t mode) {
   cg::grid_group grid = cg::this_grid();
@@ -2456,11 +2515,12 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(const __grid_con
     device_loop(d, grid, sm, clk, RK_PUSH, true, false);
     // part from the final fresh BFS (S = unreached = S_max, R15) + flow (R8)
     long long f = 0;
-    for (int32_t v = gt; v < n; v += nt) {
-      d.part[v] = ldv(d.hp + v) < n ? PART_T : PART_S;
-      const long long ev = ldv(d.e + v);
-      f += v == d.t ? ev : (v != d.s && ev < 0 ? ev : 0);
-    }
+    vsweep<VX>(n, [&](int32_t v) { return VX{ldv(d.e + v), ldv(d.hp + v), 0}; },
+               [&](int32_t v, const VX &x, bool ok) {
+                 if (!ok) return;
+                 d.part[v] = x.hp < n ? PART_T : PART_S;
+                 f += v == d.t ? x.e : (v != d.s && x.e < 0 ? x.e : 0);
+               });
     f = bg.sum(f);
     if (threadIdx.x == 0 && f) atomicAdd(reinterpret_cast<unsigned long long *>(&ctl->flow), (unsigned long long)f);
   } else if (mode == MODE_PP) {
@@ -2479,23 +2539,24 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(const __grid_con
         for (int i = threadIdx.x; i < 2 * GAPW; i += NTHREADS) hist[i] = 0;
         __syncthreads();
       }
-      for (int32_t v = gt; v < n; v += nt) {
-        const long long ev = ldv(d.e + v);
-        f += v == d.t ? ev : (v != d.s && ev < 0 ? ev : 0);
-        const int32_t hpv = ldv(d.hp + v);
-        int32_t hmv = ldv(d.hm + v);
-        const bool tside = hpv < n;                // reaches t or a deficit: T' (R15)
-        d.part[v] = tside ? PART_T : PART_S;
-        if (tside) { d.hm[v] = n + 1; hmv = n + 1; }
-        else {
-          d.hp[v] = n + 1;
-          if (hmv > n) { d.hm[v] = n; hmv = n; }  // (T -> S': in the pull region, unreached)
+      vsweep<VX>(n, [&](int32_t v) { return VX{ldv(d.e + v), ldv(d.hp + v), ldv(d.hm + v)}; },
+                 [&](int32_t v, const VX &x, bool ok) {
+        int32_t hmv = x.hm;
+        if (ok) {
+          f += v == d.t ? x.e : (v != d.s && x.e < 0 ? x.e : 0);
+          const bool tside = x.hp < n;             // reaches t or a deficit: T' (R15)
+          d.part[v] = tside ? PART_T : PART_S;
+          if (tside) { d.hm[v] = n + 1; hmv = n + 1; }
+          else {
+            d.hp[v] = n + 1;
+            if (hmv > n) { d.hm[v] = n; hmv = n; }  // (T -> S': in the pull region, unreached)
+          }
         }
         if (want_hist) {
-          if (hpv < n && hpv < GAPW) atomicAdd(hist + hpv, 1);
-          if (hmv < n && hmv < GAPW) atomicAdd(hist + GAPW + hmv, 1);
+          hist_add(hist, ok && x.hp < n && x.hp < GAPW, x.hp);
+          hist_add(hist + GAPW, ok && hmv < n && hmv < GAPW, hmv);
         }
-      }
+      });
       f = bg.sum(f);
       if (threadIdx.x == 0 && f) atomicAdd(reinterpret_cast<unsigned long long *>(&ctl->flow), (unsigned long long)f);
       if (blockIdx.x == 0 && threadIdx.x == 0) ctl->lazy_ok = 1;
@@ -2586,17 +2647,17 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(const __grid_con
       for (int i = threadIdx.x; i < 2 * GAPW; i += NTHREADS) hist[i] = 0;
       __syncthreads();
     }
-    for (int32_t v = gt; v < n; v += nt) {
-      const long long ev = ldv(d.e + v);
-      f += v == d.t ? ev : (v != d.s && ev < 0 ? ev : 0);
-      const int32_t hmv = ldv(d.hm + v);
-      d.mask[v] = hmv < n ? 1 : 0;               // S_min, cached for dmf_min_cut_source_side
-      if (want_hist) {
-        const int32_t hpv = ldv(d.hp + v);
-        if (hpv < n && hpv < GAPW) atomicAdd(hist + hpv, 1);
-        if (hmv < n && hmv < GAPW) atomicAdd(hist + GAPW + hmv, 1);
+    vsweep<VX>(n, [&](int32_t v) { return VX{ldv(d.e + v), want_hist ? ldv(d.hp + v) : 0, ldv(d.hm + v)}; },
+               [&](int32_t v, const VX &x, bool ok) {
+      if (ok) {
+        f += v == d.t ? x.e : (v != d.s && x.e < 0 ? x.e : 0);
+        d.mask[v] = x.hm < n ? 1 : 0;            // S_min, cached for dmf_min_cut_source_side
       }
-    }
+      if (want_hist) {
+        hist_add(hist, ok && x.hp < n && x.hp < GAPW, x.hp);
+        hist_add(hist + GAPW, ok && x.hm < n && x.hm < GAPW, x.hm);
+      }
+    });
     f = bg.sum(f);
     if (threadIdx.x == 0 && f) atomicAdd(reinterpret_cast<unsigned long long *>(&ctl->flow), (unsigned long long)f);
     if (want_hist) {
@@ -2637,15 +2698,14 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(const __grid_con
       for (int i = threadIdx.x; i < 2 * GAPW; i += NTHREADS) hist[i] = 0;
       __syncthreads();
     }
-    for (int32_t v = gt; v < n; v += nt) {
-      const int32_t hmv = ldv(d.hm + v);
-      d.mask[v] = mode == MODE_MINCUT ? (hmv < n ? 1 : 0) : (ldv(d.hp + v) < n ? 0 : 1);
+    vsweep<VX>(n, [&](int32_t v) { return VX{0, ldv(d.hp + v), ldv(d.hm + v)}; },
+               [&](int32_t v, const VX &x, bool ok) {
+      if (ok) d.mask[v] = mode == MODE_MINCUT ? (x.hm < n ? 1 : 0) : (x.hp < n ? 0 : 1);
       if (want_hist) {
-        const int32_t hpv = ldv(d.hp + v);
-        if (hpv < n && hpv < GAPW) atomicAdd(hist + hpv, 1);
-        if (hmv < n && hmv < GAPW) atomicAdd(hist + GAPW + hmv, 1);
+        hist_add(hist, ok && x.hp < n && x.hp < GAPW, x.hp);
+        hist_add(hist + GAPW, ok && x.hm < n && x.hm < GAPW, x.hm);
       }
-    }
+    });
     if (want_hist) {
       __syncthreads();
       for (int i = threadIdx.x; i < 2 * GAPW; i += NTHREADS)
