@@ -9,6 +9,7 @@
 #include "dmf.h"
 #include "dmf_device.cuh"
 #include "solve.cuh"
+#include "reach.cuh"
 
 #include <cub/cub.cuh>
 
@@ -100,6 +101,8 @@ struct dmf_graph {
   int32_t trace_cap = 0;
   int32_t *ddbg = nullptr;   // device view
   int grid_blocks = 0;
+  int reach_blocks = 0;      // cooperative grid of k_reach (S_min query)
+  bool reach = true;         // DMF_REACH=0: the S_min query runs k_solve's MINCUT mode instead
   double watchdog_s = 0;
   int32_t batch_id = 0;
   bool solved = false;
@@ -357,7 +360,12 @@ static int run_solve(dmf_graph *g, int32_t mode, const Dev &dv) {
   d.async = (mode == MODE_STATIC ? g->async_static : g->async) ? 1 : 0;
   int32_t md = mode;
   void *args[] = {&d, &md};
-  CK(cudaLaunchCooperativeKernel((const void *)k_solve<NT>, dim3(g->grid_blocks), dim3(NT), args, 0, g->stream));
+  if (mode == MODE_MINCUT && g->reach) {
+    void *rargs[] = {&d};
+    CK(cudaLaunchCooperativeKernel((const void *)k_reach, dim3(g->reach_blocks), dim3(RNT), rargs, 0, g->stream));
+  } else {
+    CK(cudaLaunchCooperativeKernel((const void *)k_solve<NT>, dim3(g->grid_blocks), dim3(NT), args, 0, g->stream));
+  }
   g->launches++;
   CK(cudaEventRecord(g->ev1, g->stream));
   CK(cudaMemcpyAsync(g->hctl, g->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, g->stream));
@@ -634,7 +642,7 @@ int dmf_create(int32_t n, const int64_t *row_ptr, const int32_t *col, const int3
     if (const char *ia = getenv("DMF_IMM_ACT")) g->imm_act = atoi(ia) != 0;
     if (const char *s2 = getenv("DMF_SCAN2")) g->scan2 = atoi(s2) != 0;
     g->check_level = knob(o.check_level, "DMF_CHECK_LEVEL");
-    if (const char *ba = getenv("DMF_BU_ALPHA")) g->bu_alpha = atoi(ba) > 0 ? atoi(ba) : g->bu_alpha;
+    if (const char *ba = getenv("DMF_BU_ALPHA")) g->bu_alpha = atoi(ba) >= 0 ? atoi(ba) : g->bu_alpha;   // 0: never bottom-up
     if (const char *dd = getenv("DMF_DENSE_DIV")) g->dense_div = atoi(dd) > 0 ? atoi(dd) : g->dense_div;
     if (const char *sl = getenv("DMF_ASYNC_SLEEP_NS")) g->async_sleep_ns = atoi(sl) > 0 ? atoi(sl) : 128;
     for (int i = 0; i < 7; i++)
@@ -702,6 +710,13 @@ int dmf_create(int32_t n, const int64_t *row_ptr, const int32_t *col, const int3
   if (per_sm < 1) { fail(DMF_ECUDA, "solve kernel cannot be resident (occupancy 0)"); return bail(DMF_ECUDA); }
   g->grid_blocks = per_sm * sms;
   if (g->opt.grid_blocks > 0 && g->opt.grid_blocks < g->grid_blocks) g->grid_blocks = g->opt.grid_blocks;
+  {
+    int rper = 0;
+    CKB(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&rper, k_reach, RNT, 0));
+    if (rper < 1) { fail(DMF_ECUDA, "reach kernel cannot be resident (occupancy 0)"); return bail(DMF_ECUDA); }
+    g->reach_blocks = rper * sms;
+    if (const char *rc = getenv("DMF_REACH")) g->reach = atoi(rc) != 0;
+  }
   CKB(cudaEventCreate(&g->ev0));
   CKB(cudaEventCreate(&g->ev1));
   g->stats.n = n; g->stats.m = g->m; g->stats.S = S; g->stats.kernel_cycles = g->kc;

@@ -87,6 +87,12 @@ struct Ctl {
   int32_t pdef, pexc;           // DYN_PP: deficit / excess vertices in P (stage 2 / P-reach skip)
   int32_t sreach;               // DYN_PP certificate: s reaches a vertex labelled by the backward BFS
   int32_t lazy_ok;              // DYN_PP: converged by the certificate (no S_min mask computed)
+  // S_min query (k_reach, reach.cuh): per level % 3
+  int32_t rcnt[3];              // frontier items of the level
+  int32_t rnv[3];               // vertices labelled with the level
+  int32_t rbq[3];               // bottom-up: rows queued for the warp pass
+  unsigned long long rfs[3];    // slots of the level's vertices
+  unsigned long long rmu;       // slots of the vertices not labelled at level 0
 };
 
 // Everything a kernel needs, passed by value.  Slot arrays are SoA int32[S]:

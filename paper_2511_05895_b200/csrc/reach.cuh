@@ -1,0 +1,348 @@
+// reach.cuh -- the S_min query (dmf_min_cut_source_side, reading R19):
+// S_min is the set of vertices reachable from {s} u {v != t : e(v) > 0} in the residual
+// graph of the converged state (c_f(u,v) = res[slot (u,v)] > 0).  It is the
+// intersection of all minimum cuts' source sides, unique, and it does not depend on
+// which maximum (pre)flow the engine holds.
+//
+// A lean level-synchronous, direction-optimising BFS in its OWN persistent cooperative
+// kernel: 256 threads and <= 40 registers per thread, i.e. 48 resident warps per SM --
+// 1.5x the warps k_solve can keep resident -- because a BFS level is a chain of
+// dependent loads (row -> slot -> neighbour height) whose throughput is set by how
+// many such chains are in flight.  It writes
+//   * hm[v] = the exact BFS distance from the roots (|V| if unreached): the pull-track
+//     labels a following DYN_PP warm start discharges on (as k_solve's MINCUT did),
+//   * mask[v] = hm[v] < |V|,
+//   * the level histogram of the warm start's local gap (R14 form 2) into cnt_next
+//     (hm half = the level sizes; hp half copied from cnt: hp is unchanged here).
+// Top-down levels claim by atomicCAS(hm, |V|, L+1) over frontier items of <= RCH slots
+// (hub rows split, so that no warp serialises a level); bottom-up levels (frontier
+// slots x RALPHA > slots still unvisited) let every unvisited vertex look for an
+// in-neighbour at level L with residual towards it, thread-serial for short rows, a warp
+// with early exit for longer ones.
+#pragma once
+
+#include "dmf_device.cuh"
+
+namespace dmf {
+
+constexpr int RNT = 256;                    // threads per CTA
+#ifndef DMF_RMINB
+#define DMF_RMINB 6
+#endif
+constexpr int RMINB = DMF_RMINB;            // resident CTAs per SM (6: <= 40 registers, 48 warps)
+constexpr int RWPB = RNT / 32;
+constexpr int32_t RCH = 1024;               // top-down: slots per frontier item
+constexpr int32_t RBU_T = 24;               // bottom-up: rows of more slots go to the warp pass
+constexpr unsigned long long RALPHA = 2;    // bottom-up iff frontier slots x RALPHA > unvisited slots
+constexpr unsigned long long RDENSE_DIV = 64;   // dense top-down iff frontier slots x RDENSE_DIV >= S
+
+constexpr int32_t RSTG = 1024;              // frontier items staged per CTA (flushed once per phase)
+constexpr int32_t RQSTG = 256;              // bottom-up warp-pass candidates staged per CTA
+
+struct RSm {
+  long long red[RWPB];
+  unsigned long long tclk;
+  long long it[RSTG];                       // staged frontier items
+  int32_t q[RQSTG];                         // staged bottom-up warp-pass candidates
+  int32_t icnt, qcnt, ibase, qbase;
+};
+
+__device__ __forceinline__ long long r_bsum(RSm &sm, long long x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) sm.red[threadIdx.x >> 5] = x;
+  __syncthreads();
+  long long r = 0;
+#pragma unroll
+  for (int i = 0; i < RWPB; i++) r += sm.red[i];
+  return r;
+}
+
+// block 0 / thread 0: charge the time since the last lap to stat `which` (and write a
+// phase trace record when tracing, same layout as k_solve's PhaseClock)
+__device__ __forceinline__ void r_lap(const Dev &d, RSm &sm, int which, int32_t sub = 0, int32_t items = 0,
+                                      int32_t extra = 0) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const unsigned long long now = gtimer();
+    d.ctl->stat[which] += now - sm.tclk;
+    if (d.trace && d.ctl->ntrace < d.trace_cap) {
+      int32_t *rec = d.trace + 8 * d.ctl->ntrace++;
+      rec[0] = which - ST_T_PRO; rec[1] = 0; rec[2] = sub; rec[3] = items; rec[4] = extra;
+      rec[5] = (int32_t)(now - sm.tclk); rec[6] = 0; rec[7] = 0;
+    }
+    sm.tclk = now;
+  }
+}
+
+// warp-convergent: lanes with pred append v's row as ceil(deg / RCH) frontier items,
+// staged in shared memory (a returning global atomic per warp on ONE counter serialises
+// every appending warp of the grid in one L2 slice); overflow goes to the global list
+__device__ __forceinline__ void r_append(RSm &sm, long long *list, int32_t *cnt, bool pred, int32_t v, int32_t deg) {
+  const int32_t nit = pred ? (deg + RCH - 1) / RCH : 0;
+  if (__ballot_sync(0xffffffffu, nit > 0) == 0) return;
+  const int lane = threadIdx.x & 31;
+  int32_t inc = nit;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  // positions base.. of the CTA's stage; those at >= RSTG go to a global range of the
+  // overflow's size (so that the first RSTG stage positions are always all written)
+  int32_t base = 0, gb = 0;
+  if (lane == 31) {
+    base = atomicAdd(&sm.icnt, inc);
+    const int32_t over = base + inc - max(base, RSTG);
+    if (over > 0) gb = atomicAdd(cnt, over) - max(base, RSTG);
+  }
+  base = __shfl_sync(0xffffffffu, base, 31) + inc - nit;
+  gb = __shfl_sync(0xffffffffu, gb, 31);
+  for (int32_t k = 0; k < nit; k++) {
+    const long long e = ((long long)k << 32) | (long long)(uint32_t)v;
+    if (base + k < RSTG) sm.it[base + k] = e;
+    else list[gb + base + k] = e;
+  }
+}
+// warp-convergent: stage a bottom-up warp-pass candidate
+__device__ __forceinline__ void r_queue(RSm &sm, int32_t *q, int32_t *qc, bool pred, int32_t v) {
+  const unsigned m = __ballot_sync(0xffffffffu, pred);
+  if (m == 0) return;
+  const int lane = threadIdx.x & 31, lead = __ffs(m) - 1;
+  int32_t base = 0, gb = 0;
+  if (lane == lead) {
+    base = atomicAdd(&sm.qcnt, __popc(m));
+    const int32_t over = base + __popc(m) - max(base, RQSTG);
+    if (over > 0) gb = atomicAdd(qc, over) - max(base, RQSTG);
+  }
+  gb = __shfl_sync(0xffffffffu, gb, lead);
+  base = __shfl_sync(0xffffffffu, base, lead) + __popc(m & ((1u << lane) - 1u));
+  if (pred) { if (base < RQSTG) sm.q[base] = v; else q[gb + base] = v; }
+}
+// block-wide: move the staged items / candidates to the global lists (one atomic each)
+__device__ __forceinline__ void r_flush(RSm &sm, long long *list, int32_t *cnt, int32_t *q, int32_t *qc) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int32_t a = min(sm.icnt, RSTG), b = min(sm.qcnt, RQSTG);
+    sm.icnt = a; sm.qcnt = b;
+    sm.ibase = a ? atomicAdd(cnt, a) : 0;
+    sm.qbase = b ? atomicAdd(qc, b) : 0;
+  }
+  __syncthreads();
+  for (int32_t x = threadIdx.x; x < sm.icnt; x += RNT) list[sm.ibase + x] = sm.it[x];
+  for (int32_t x = threadIdx.x; x < sm.qcnt; x += RNT) q[sm.qbase + x] = sm.q[x];
+  __syncthreads();
+  if (threadIdx.x == 0) { sm.icnt = 0; sm.qcnt = 0; }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(RNT, RMINB) k_reach(const __grid_constant__ Dev d) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ RSm sm;
+  Ctl *ctl = d.ctl;
+  const int32_t n = d.n;
+  const int lane = threadIdx.x & 31;
+  const int32_t nt = gridDim.x * RNT;
+  const int32_t gw = (int32_t)((threadIdx.x >> 5) * gridDim.x + blockIdx.x), nw = gridDim.x * RWPB;
+  const bool want_hist = d.local_gap && d.cnt_next;
+  if (threadIdx.x == 0) { sm.tclk = gtimer(); sm.icnt = 0; sm.qcnt = 0; }
+  __syncthreads();
+  if (blockIdx.x == 0 && want_hist)
+    for (int i = threadIdx.x; i < GAPW; i += RNT) { d.cnt_next[i] = d.cnt[i]; d.cnt_next[GAPW + i] = 0; }
+
+  // ---- roots: level 0 = {s} u {v != t : e(v) > 0}; everything else |V|
+  {
+    long long fdeg = 0, udeg = 0, nroot = 0;
+    for (int32_t t0 = blockIdx.x * RNT * 4; t0 < n; t0 += nt * 4) {
+      long long ev[4];
+      int32_t dg[4];
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        const int32_t v = t0 + j * RNT + threadIdx.x;
+        ev[j] = v < n ? ldv(d.e + v) : 0;
+        dg[j] = v < n ? d.row[v + 1] - d.row[v] : 0;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        const int32_t v = t0 + j * RNT + threadIdx.x;
+        const bool root = v < n && (v == d.s || (v != d.t && ev[j] > 0));
+        if (v < n) d.hm[v] = root ? 0 : n;
+        if (root) { fdeg += dg[j]; nroot++; }
+        else if (v < n && v != d.t) udeg += dg[j];
+        r_append(sm, d.cq0, &ctl->rcnt[0], root, v, dg[j]);
+      }
+    }
+    r_flush(sm, d.cq0, &ctl->rcnt[0], d.bul, &ctl->rbq[0]);
+    fdeg = r_bsum(sm, fdeg); udeg = r_bsum(sm, udeg); nroot = r_bsum(sm, nroot);
+    if (threadIdx.x == 0) {
+      if (fdeg) atomicAdd(&ctl->rfs[0], (unsigned long long)fdeg);
+      if (udeg) atomicAdd(&ctl->rmu, (unsigned long long)udeg);
+      if (nroot) atomicAdd(&ctl->rnv[0], (int32_t)nroot);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) d.ctl->stat[ST_RESET_V] += (unsigned long long)n;
+  }
+  grid.sync();
+  r_lap(d, sm, ST_T_RESET, 0, n);
+
+  unsigned long long mu = ldv(reinterpret_cast<const long long *>(&ctl->rmu));
+  for (int32_t L = 0;; ++L) {
+    const int cur = L % 3, nx = (L + 1) % 3, nn = (L + 2) % 3;
+    const int32_t nv = ldv(&ctl->rnv[cur]);
+    if (nv == 0) break;                            // nothing labelled at level L: done
+    const int32_t cnt = ldv(&ctl->rcnt[cur]);
+    const unsigned long long f = (unsigned long long)ldv(reinterpret_cast<const long long *>(&ctl->rfs[cur]));
+    if (L > 0) mu = mu > f ? mu - f : 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {    // slot nn was last read in level L-1
+      ctl->rcnt[nn] = 0; ctl->rfs[nn] = 0; ctl->rnv[nn] = 0; ctl->rbq[nn] = 0;
+      if (want_hist && L < GAPW) d.cnt_next[GAPW + L] = nv;
+      ctl->stat[ST_LEVELS] += 1;
+      ctl->stat[ST_BFS_V] += (unsigned long long)nv;
+    }
+    const long long *cl = (L & 1) ? d.cq1 : d.cq0;
+    long long *nl = (L & 1) ? d.cq0 : d.cq1;
+    long long fdeg = 0, nlab = 0;
+    const bool bu = f * RALPHA > mu;
+    // dense top-down: a frontier of >= S / RDENSE_DIV slots discovers most vertices many
+    // times over -- label by idempotent stores, then build the next frontier by a sweep
+    const bool dense = !bu && f * RDENSE_DIV >= (unsigned long long)d.S;
+    if (!bu) {
+      // ---- top-down: warp per frontier item, 4 slots per lane per step
+      for (int32_t x = gw; x < cnt; x += nw) {
+        const long long it = cl[x];
+        const int32_t u = (int32_t)(uint32_t)it;
+        const int32_t beg = d.row[u] + (int32_t)(it >> 32) * RCH;
+        const int32_t end = min(d.row[u + 1], beg + RCH);
+        for (int32_t b = beg; b < end; b += 128) {
+          int32_t r[4], w[4];
+#pragma unroll
+          for (int j = 0; j < 4; j++) {
+            const int32_t i = b + j * 32 + lane;
+            r[j] = i < end ? ldv(d.res + i) : 0;
+            w[j] = i < end ? d.dst[i] : 0;
+          }
+#pragma unroll
+          for (int j = 0; j < 4; j++)          // stale |V| is harmless: the CAS / the sweep decides
+#ifdef DMF_RDENSE_CG
+            r[j] = (r[j] > 0 && w[j] != d.t && (dense ? ldv(d.hm + w[j]) : ldl1(d.hm + w[j])) == n) ? 1 : 0;
+#else
+            r[j] = (r[j] > 0 && w[j] != d.t && ldl1(d.hm + w[j]) == n) ? 1 : 0;
+#endif
+          if (dense) {
+#pragma unroll
+            for (int j = 0; j < 4; j++) if (r[j]) d.hm[w[j]] = L + 1;
+            continue;
+          }
+#pragma unroll
+          for (int j = 0; j < 4; j++) r[j] = r[j] && atomicCAS(d.hm + w[j], n, L + 1) == n;
+          int32_t dg[4];
+#pragma unroll
+          for (int j = 0; j < 4; j++) dg[j] = r[j] ? d.row[w[j] + 1] - d.row[w[j]] : 0;
+#pragma unroll
+          for (int j = 0; j < 4; j++) {
+            if (r[j]) { fdeg += dg[j]; nlab++; }
+            r_append(sm, nl, &ctl->rcnt[nx], r[j] != 0, w[j], dg[j]);
+          }
+        }
+      }
+      if (dense) {
+        grid.sync();
+        // ---- the next frontier = {v : hm[v] = L+1}
+        for (int32_t t0 = blockIdx.x * RNT * 4; t0 < n; t0 += nt * 4) {
+          int32_t h[4], dg[4];
+#pragma unroll
+          for (int j = 0; j < 4; j++) {
+            const int32_t v = t0 + j * RNT + threadIdx.x;
+            h[j] = v < n ? ldv(d.hm + v) : n;
+          }
+#pragma unroll
+          for (int j = 0; j < 4; j++) {
+            const int32_t v = t0 + j * RNT + threadIdx.x;
+            dg[j] = h[j] == L + 1 ? d.row[v + 1] - d.row[v] : 0;
+          }
+#pragma unroll
+          for (int j = 0; j < 4; j++) {
+            const int32_t v = t0 + j * RNT + threadIdx.x;
+            if (h[j] == L + 1) { fdeg += dg[j]; nlab++; }
+            r_append(sm, nl, &ctl->rcnt[nx], h[j] == L + 1, v, dg[j]);
+          }
+        }
+      }
+    } else {
+      if (blockIdx.x == 0 && threadIdx.x == 0) ctl->stat[ST_BU_LEVELS] += 1;
+      // ---- bottom-up pass A: thread per unvisited vertex with a short row
+      for (int32_t v = blockIdx.x * RNT + threadIdx.x; v - (int32_t)threadIdx.x < n; v += nt) {
+        const bool in = v < n;
+        const int32_t h = in ? ldv(d.hm + v) : 0;
+        const int32_t rb = in ? d.row[v] : 0, re = in ? d.row[v + 1] : 0;
+        const bool cand = in && h == n && v != d.t;
+        const bool big = cand && re - rb > RBU_T;
+        bool found = false;
+        if (cand && !big) {
+          for (int32_t i0 = rb; i0 < re && !found; i0 += 4) {
+            int32_t r[4], w[4];
+#pragma unroll
+            for (int j = 0; j < 4; j++) {      // in-slot (v,u): rres = c_f(u,v)
+              r[j] = i0 + j < re ? ldv(d.rres + i0 + j) : 0;
+              w[j] = i0 + j < re ? d.dst[i0 + j] : 0;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; j++) found |= r[j] > 0 && ldl1(d.hm + w[j]) == L;   // level-L labels are frozen
+          }
+          if (found) { d.hm[v] = L + 1; fdeg += re - rb; nlab++; }
+        }
+        r_queue(sm, d.bul, &ctl->rbq[cur], big, v);
+        r_append(sm, nl, &ctl->rcnt[nx], found, v, re - rb);
+      }
+      r_flush(sm, nl, &ctl->rcnt[nx], d.bul, &ctl->rbq[cur]);
+      grid.sync();
+      // ---- pass B: warp per queued vertex, early exit on the first in-neighbour at L
+      const int32_t q = ldv(&ctl->rbq[cur]);
+      for (int32_t x = gw; x < q; x += nw) {
+        const int32_t v = d.bul[x];
+        const int32_t rb = d.row[v], re = d.row[v + 1];
+        bool found = false;
+        for (int32_t b = rb; b < re; b += 128) {
+          int32_t r[4], w[4];
+#pragma unroll
+          for (int j = 0; j < 4; j++) {
+            const int32_t i = b + j * 32 + lane;
+            r[j] = i < re ? ldv(d.rres + i) : 0;
+            w[j] = i < re ? d.dst[i] : 0;
+          }
+          bool hit = false;
+#pragma unroll
+          for (int j = 0; j < 4; j++) hit |= r[j] > 0 && ldl1(d.hm + w[j]) == L;
+          if (__any_sync(0xffffffffu, hit)) { found = true; break; }
+        }
+        if (found && lane == 0) { d.hm[v] = L + 1; fdeg += re - rb; nlab++; }
+        r_append(sm, nl, &ctl->rcnt[nx], found && lane == 0, v, re - rb);
+      }
+    }
+    r_flush(sm, nl, &ctl->rcnt[nx], d.bul, &ctl->rbq[cur]);
+    fdeg = r_bsum(sm, fdeg); nlab = r_bsum(sm, nlab);
+    if (threadIdx.x == 0) {
+      if (fdeg) atomicAdd(&ctl->rfs[nx], (unsigned long long)fdeg);
+      if (nlab) atomicAdd(&ctl->rnv[nx], (int32_t)nlab);
+    }
+    grid.sync();
+    r_lap(d, sm, ST_T_BFS, L, nv, (bu ? 2 : 0) | (dense ? 4 : 0) | (cnt << 3));
+  }
+
+  // ---- the S_min mask
+  for (int32_t t0 = blockIdx.x * RNT * 4; t0 < n; t0 += nt * 4) {
+    int32_t h[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const int32_t v = t0 + j * RNT + threadIdx.x;
+      h[j] = v < n ? ldv(d.hm + v) : n;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const int32_t v = t0 + j * RNT + threadIdx.x;
+      if (v < n) d.mask[v] = h[j] < n ? 1 : 0;
+    }
+  }
+  r_lap(d, sm, ST_T_EPI);
+}
+
+}  // namespace dmf
