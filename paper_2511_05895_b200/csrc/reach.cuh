@@ -14,8 +14,10 @@
 //   * mask[v] = hm[v] < |V|,
 //   * the level histogram of the warm start's local gap (R14 form 2) into cnt_next
 //     (hm half = the level sizes; hp half copied from cnt: hp is unchanged here).
-// Top-down levels claim by atomicCAS(hm, |V|, L+1) over frontier items of <= RCH slots
-// (hub rows split, so that no warp serialises a level); bottom-up levels (frontier
+// Top-down levels claim by atomicCAS(hm, |V|, L+1) over frontier items, slot ranges of
+// <= RCH slots (hub rows split, so that no warp serialises a level; no row lookup per
+// item), or by idempotent stores and a sweep for the next frontier when the frontier is
+// dense; bottom-up levels (frontier
 // slots x RALPHA > slots still unvisited) let every unvisited vertex look for an
 // in-neighbour at level L with residual towards it, thread-serial for short rows, a warp
 // with early exit for longer ones.
@@ -31,9 +33,15 @@ constexpr int RNT = 256;                    // threads per CTA
 #endif
 constexpr int RMINB = DMF_RMINB;            // resident CTAs per SM (6: <= 40 registers, 48 warps)
 constexpr int RWPB = RNT / 32;
-constexpr int32_t RCH = 1024;               // top-down: slots per frontier item
+#ifndef DMF_RCH
+#define DMF_RCH 256
+#endif
+#ifndef DMF_RALPHA
+#define DMF_RALPHA 2
+#endif
+constexpr int32_t RCH = DMF_RCH;            // top-down: slots per frontier item
 constexpr int32_t RBU_T = 24;               // bottom-up: rows of more slots go to the warp pass
-constexpr unsigned long long RALPHA = 2;    // bottom-up iff frontier slots x RALPHA > unvisited slots
+constexpr unsigned long long RALPHA = DMF_RALPHA;   // bottom-up iff frontier slots x RALPHA > unvisited slots
 constexpr unsigned long long RDENSE_DIV = 64;   // dense top-down iff frontier slots x RDENSE_DIV >= S
 
 constexpr int32_t RSTG = 1024;              // frontier items staged per CTA (flushed once per phase)
@@ -75,10 +83,12 @@ __device__ __forceinline__ void r_lap(const Dev &d, RSm &sm, int which, int32_t 
   }
 }
 
-// warp-convergent: lanes with pred append v's row as ceil(deg / RCH) frontier items,
+// warp-convergent: lanes with pred append the row [rb, rb + deg) of a labelled vertex as
+// ceil(deg / RCH) frontier items, each a slot range (end << 32 | begin): a top-down
+// level then needs no row lookup per item.  Items are
 // staged in shared memory (a returning global atomic per warp on ONE counter serialises
 // every appending warp of the grid in one L2 slice); overflow goes to the global list
-__device__ __forceinline__ void r_append(RSm &sm, long long *list, int32_t *cnt, bool pred, int32_t v, int32_t deg) {
+__device__ __forceinline__ void r_append(RSm &sm, long long *list, int32_t *cnt, bool pred, int32_t rb, int32_t deg) {
   const int32_t nit = pred ? (deg + RCH - 1) / RCH : 0;
   if (__ballot_sync(0xffffffffu, nit > 0) == 0) return;
   const int lane = threadIdx.x & 31;
@@ -99,7 +109,8 @@ __device__ __forceinline__ void r_append(RSm &sm, long long *list, int32_t *cnt,
   base = __shfl_sync(0xffffffffu, base, 31) + inc - nit;
   gb = __shfl_sync(0xffffffffu, gb, 31);
   for (int32_t k = 0; k < nit; k++) {
-    const long long e = ((long long)k << 32) | (long long)(uint32_t)v;
+    const int32_t b = rb + k * RCH;
+    const long long e = ((long long)min(rb + deg, b + RCH) << 32) | (long long)(uint32_t)b;
     if (base + k < RSTG) sm.it[base + k] = e;
     else list[gb + base + k] = e;
   }
@@ -155,12 +166,13 @@ __global__ void __launch_bounds__(RNT, RMINB) k_reach(const __grid_constant__ De
     long long fdeg = 0, udeg = 0, nroot = 0;
     for (int32_t t0 = blockIdx.x * RNT * 4; t0 < n; t0 += nt * 4) {
       long long ev[4];
-      int32_t dg[4];
+      int32_t rb[4], dg[4];
 #pragma unroll
       for (int j = 0; j < 4; j++) {
         const int32_t v = t0 + j * RNT + threadIdx.x;
         ev[j] = v < n ? ldv(d.e + v) : 0;
-        dg[j] = v < n ? d.row[v + 1] - d.row[v] : 0;
+        rb[j] = v < n ? d.row[v] : 0;
+        dg[j] = v < n ? d.row[v + 1] - rb[j] : 0;
       }
 #pragma unroll
       for (int j = 0; j < 4; j++) {
@@ -169,7 +181,7 @@ __global__ void __launch_bounds__(RNT, RMINB) k_reach(const __grid_constant__ De
         if (v < n) d.hm[v] = root ? 0 : n;
         if (root) { fdeg += dg[j]; nroot++; }
         else if (v < n && v != d.t) udeg += dg[j];
-        r_append(sm, d.cq0, &ctl->rcnt[0], root, v, dg[j]);
+        r_append(sm, d.cq0, &ctl->rcnt[0], root, rb[j], dg[j]);
       }
     }
     r_flush(sm, d.cq0, &ctl->rcnt[0], d.bul, &ctl->rbq[0]);
@@ -185,11 +197,15 @@ __global__ void __launch_bounds__(RNT, RMINB) k_reach(const __grid_constant__ De
   r_lap(d, sm, ST_T_RESET, 0, n);
 
   unsigned long long mu = ldv(reinterpret_cast<const long long *>(&ctl->rmu));
+  // The item list of level L exists only if level L-1 was a sparse top-down level (its
+  // claims append) or L = 0; after a dense or bottom-up level it is built by a sweep
+  // only if level L goes top-down (usually the level after those goes bottom-up).
+  bool built = true;
   for (int32_t L = 0;; ++L) {
     const int cur = L % 3, nx = (L + 1) % 3, nn = (L + 2) % 3;
     const int32_t nv = ldv(&ctl->rnv[cur]);
     if (nv == 0) break;                            // nothing labelled at level L: done
-    const int32_t cnt = ldv(&ctl->rcnt[cur]);
+    int32_t cnt = ldv(&ctl->rcnt[cur]);
     const unsigned long long f = (unsigned long long)ldv(reinterpret_cast<const long long *>(&ctl->rfs[cur]));
     if (L > 0) mu = mu > f ? mu - f : 0;
     if (blockIdx.x == 0 && threadIdx.x == 0) {    // slot nn was last read in level L-1
@@ -198,20 +214,41 @@ __global__ void __launch_bounds__(RNT, RMINB) k_reach(const __grid_constant__ De
       ctl->stat[ST_LEVELS] += 1;
       ctl->stat[ST_BFS_V] += (unsigned long long)nv;
     }
-    const long long *cl = (L & 1) ? d.cq1 : d.cq0;
+    long long *cl = (L & 1) ? d.cq1 : d.cq0;
     long long *nl = (L & 1) ? d.cq0 : d.cq1;
     long long fdeg = 0, nlab = 0;
     const bool bu = f * RALPHA > mu;
+    if (!bu && !built) {                           // the level's items: {v : hm[v] = L}
+      for (int32_t t0 = blockIdx.x * RNT * 4; t0 < n; t0 += nt * 4) {
+        int32_t h[4], rb[4], dg[4];
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+          const int32_t v = t0 + j * RNT + threadIdx.x;
+          h[j] = v < n ? ldv(d.hm + v) : n;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+          const int32_t v = t0 + j * RNT + threadIdx.x;
+          rb[j] = h[j] == L ? d.row[v] : 0;
+          dg[j] = h[j] == L ? d.row[v + 1] - rb[j] : 0;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; j++) r_append(sm, cl, &ctl->rcnt[cur], h[j] == L, rb[j], dg[j]);
+      }
+      r_flush(sm, cl, &ctl->rcnt[cur], d.bul, &ctl->rbq[cur]);
+      grid.sync();
+      cnt = ldv(&ctl->rcnt[cur]);
+    }
     // dense top-down: a frontier of >= S / RDENSE_DIV slots discovers most vertices many
     // times over -- label by idempotent stores, then build the next frontier by a sweep
     const bool dense = !bu && f * RDENSE_DIV >= (unsigned long long)d.S;
     if (!bu) {
       // ---- top-down: warp per frontier item, 4 slots per lane per step
+      long long itn = gw < cnt ? cl[gw] : 0;     // next item, loaded one item ahead
       for (int32_t x = gw; x < cnt; x += nw) {
-        const long long it = cl[x];
-        const int32_t u = (int32_t)(uint32_t)it;
-        const int32_t beg = d.row[u] + (int32_t)(it >> 32) * RCH;
-        const int32_t end = min(d.row[u + 1], beg + RCH);
+        const long long it = itn;
+        itn = x + nw < cnt ? cl[x + nw] : 0;
+        const int32_t beg = (int32_t)(uint32_t)it, end = (int32_t)(it >> 32);
         for (int32_t b = beg; b < end; b += 128) {
           int32_t r[4], w[4];
 #pragma unroll
@@ -222,11 +259,7 @@ __global__ void __launch_bounds__(RNT, RMINB) k_reach(const __grid_constant__ De
           }
 #pragma unroll
           for (int j = 0; j < 4; j++)          // stale |V| is harmless: the CAS / the sweep decides
-#ifdef DMF_RDENSE_CG
-            r[j] = (r[j] > 0 && w[j] != d.t && (dense ? ldv(d.hm + w[j]) : ldl1(d.hm + w[j])) == n) ? 1 : 0;
-#else
             r[j] = (r[j] > 0 && w[j] != d.t && ldl1(d.hm + w[j]) == n) ? 1 : 0;
-#endif
           if (dense) {
 #pragma unroll
             for (int j = 0; j < 4; j++) if (r[j]) d.hm[w[j]] = L + 1;
@@ -234,21 +267,25 @@ __global__ void __launch_bounds__(RNT, RMINB) k_reach(const __grid_constant__ De
           }
 #pragma unroll
           for (int j = 0; j < 4; j++) r[j] = r[j] && atomicCAS(d.hm + w[j], n, L + 1) == n;
-          int32_t dg[4];
+          int32_t rb[4], dg[4];
 #pragma unroll
-          for (int j = 0; j < 4; j++) dg[j] = r[j] ? d.row[w[j] + 1] - d.row[w[j]] : 0;
+          for (int j = 0; j < 4; j++) {
+            rb[j] = r[j] ? d.row[w[j]] : 0;
+            dg[j] = r[j] ? d.row[w[j] + 1] - rb[j] : 0;
+          }
 #pragma unroll
           for (int j = 0; j < 4; j++) {
             if (r[j]) { fdeg += dg[j]; nlab++; }
-            r_append(sm, nl, &ctl->rcnt[nx], r[j] != 0, w[j], dg[j]);
+            r_append(sm, nl, &ctl->rcnt[nx], r[j] != 0, rb[j], dg[j]);
           }
         }
       }
       if (dense) {
         grid.sync();
-        // ---- the next frontier = {v : hm[v] = L+1}
+        r_lap(d, sm, ST_T_BFS, L, nv, 4 | (cnt << 3));
+        // ---- size of the next frontier {v : hm[v] = L+1} (its items: built if needed)
         for (int32_t t0 = blockIdx.x * RNT * 4; t0 < n; t0 += nt * 4) {
-          int32_t h[4], dg[4];
+          int32_t h[4], rb[4], dg[4];
 #pragma unroll
           for (int j = 0; j < 4; j++) {
             const int32_t v = t0 + j * RNT + threadIdx.x;
@@ -257,23 +294,29 @@ __global__ void __launch_bounds__(RNT, RMINB) k_reach(const __grid_constant__ De
 #pragma unroll
           for (int j = 0; j < 4; j++) {
             const int32_t v = t0 + j * RNT + threadIdx.x;
-            dg[j] = h[j] == L + 1 ? d.row[v + 1] - d.row[v] : 0;
+            rb[j] = h[j] == L + 1 ? d.row[v] : 0;
+            dg[j] = h[j] == L + 1 ? d.row[v + 1] - rb[j] : 0;
           }
 #pragma unroll
-          for (int j = 0; j < 4; j++) {
-            const int32_t v = t0 + j * RNT + threadIdx.x;
+          for (int j = 0; j < 4; j++)
             if (h[j] == L + 1) { fdeg += dg[j]; nlab++; }
-            r_append(sm, nl, &ctl->rcnt[nx], h[j] == L + 1, v, dg[j]);
-          }
         }
       }
     } else {
       if (blockIdx.x == 0 && threadIdx.x == 0) ctl->stat[ST_BU_LEVELS] += 1;
       // ---- bottom-up pass A: thread per unvisited vertex with a short row
-      for (int32_t v = blockIdx.x * RNT + threadIdx.x; v - (int32_t)threadIdx.x < n; v += nt) {
+      // (the next vertex's label and row bounds are loaded one iteration ahead)
+      int32_t v = blockIdx.x * RNT + threadIdx.x;
+      int32_t hN = v < n ? ldv(d.hm + v) : 0, rbN = v < n ? d.row[v] : 0, reN = v < n ? d.row[v + 1] : 0;
+      for (; v - (int32_t)threadIdx.x < n; v += nt) {
         const bool in = v < n;
-        const int32_t h = in ? ldv(d.hm + v) : 0;
-        const int32_t rb = in ? d.row[v] : 0, re = in ? d.row[v + 1] : 0;
+        const int32_t h = hN, rb = rbN, re = reN;
+        {
+          const int32_t vn = v + nt;
+          hN = vn < n ? ldv(d.hm + vn) : 0;
+          rbN = vn < n ? d.row[vn] : 0;
+          reN = vn < n ? d.row[vn + 1] : 0;
+        }
         const bool cand = in && h == n && v != d.t;
         const bool big = cand && re - rb > RBU_T;
         bool found = false;
@@ -291,7 +334,6 @@ __global__ void __launch_bounds__(RNT, RMINB) k_reach(const __grid_constant__ De
           if (found) { d.hm[v] = L + 1; fdeg += re - rb; nlab++; }
         }
         r_queue(sm, d.bul, &ctl->rbq[cur], big, v);
-        r_append(sm, nl, &ctl->rcnt[nx], found, v, re - rb);
       }
       r_flush(sm, nl, &ctl->rcnt[nx], d.bul, &ctl->rbq[cur]);
       grid.sync();
@@ -315,17 +357,17 @@ __global__ void __launch_bounds__(RNT, RMINB) k_reach(const __grid_constant__ De
           if (__any_sync(0xffffffffu, hit)) { found = true; break; }
         }
         if (found && lane == 0) { d.hm[v] = L + 1; fdeg += re - rb; nlab++; }
-        r_append(sm, nl, &ctl->rcnt[nx], found && lane == 0, v, re - rb);
       }
     }
     r_flush(sm, nl, &ctl->rcnt[nx], d.bul, &ctl->rbq[cur]);
+    built = !bu && !dense;
     fdeg = r_bsum(sm, fdeg); nlab = r_bsum(sm, nlab);
     if (threadIdx.x == 0) {
       if (fdeg) atomicAdd(&ctl->rfs[nx], (unsigned long long)fdeg);
       if (nlab) atomicAdd(&ctl->rnv[nx], (int32_t)nlab);
     }
     grid.sync();
-    r_lap(d, sm, ST_T_BFS, L, nv, (bu ? 2 : 0) | (dense ? 4 : 0) | (cnt << 3));
+    r_lap(d, sm, dense ? ST_T_BFS_CMP : ST_T_BFS, L, nv, (bu ? 2 : 0) | (dense ? 4 : 0) | (cnt << 3));
   }
 
   // ---- the S_min mask
