@@ -244,8 +244,31 @@ __global__ void __launch_bounds__(RNT, RMINB) k_reach(const __grid_constant__ De
     const bool dense = !bu && f * RDENSE_DIV >= (unsigned long long)d.S;
     if (!bu) {
       // ---- top-down: warp per frontier item, 4 slots per lane per step
-      long long itn = gw < cnt ? cl[gw] : 0;     // next item, loaded one item ahead
-      for (int32_t x = gw; x < cnt; x += nw) {
+      if (dense) {
+        // labels by stores only: a whole item (<= 256 slots, 8 per lane) per step, every
+        // load of the step in flight together
+        long long itn = gw < cnt ? cl[gw] : 0;
+        for (int32_t x = gw; x < cnt; x += nw) {
+          const long long it = itn;
+          itn = x + nw < cnt ? cl[x + nw] : 0;
+          const int32_t beg = (int32_t)(uint32_t)it, end = (int32_t)(it >> 32);
+          for (int32_t b = beg; b < end; b += 256) {
+            int32_t r[8], w[8];
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+              const int32_t i = b + j * 32 + lane;
+              r[j] = i < end ? ldv(d.res + i) : 0;
+              w[j] = i < end ? d.dst[i] : 0;
+            }
+#pragma unroll
+            for (int j = 0; j < 8; j++) r[j] = r[j] > 0 && w[j] != d.t && ldl1(d.hm + w[j]) == n;
+#pragma unroll
+            for (int j = 0; j < 8; j++) if (r[j]) d.hm[w[j]] = L + 1;
+          }
+        }
+      }
+      long long itn = !dense && gw < cnt ? cl[gw] : 0;     // next item, loaded one item ahead
+      for (int32_t x = dense ? cnt : gw; x < cnt; x += nw) {
         const long long it = itn;
         itn = x + nw < cnt ? cl[x + nw] : 0;
         const int32_t beg = (int32_t)(uint32_t)it, end = (int32_t)(it >> 32);
