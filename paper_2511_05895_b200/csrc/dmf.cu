@@ -102,7 +102,8 @@ struct dmf_graph {
   int32_t *ddbg = nullptr;   // device view
   int grid_blocks = 0;
   int reach_blocks = 0;      // cooperative grid of k_reach (S_min query)
-  bool reach = true;         // DMF_REACH=0: the S_min query runs k_solve's MINCUT mode instead
+  bool reach = true;         // DMF_REACH=0: the S_min query runs k_solve's MINCUT mode and the DYN_PP
+                             // certificate runs inside k_solve instead of k_reach
   double watchdog_s = 0;
   int32_t batch_id = 0;
   bool solved = false;
@@ -362,7 +363,19 @@ static int run_solve(dmf_graph *g, int32_t mode, const Dev &dv) {
   void *args[] = {&d, &md};
   if (mode == MODE_MINCUT && g->reach) {
     void *rargs[] = {&d};
-    CK(cudaLaunchCooperativeKernel((const void *)k_reach, dim3(g->reach_blocks), dim3(RNT), rargs, 0, g->stream));
+    CK(cudaLaunchCooperativeKernel((const void *)k_reach<false>, dim3(g->reach_blocks), dim3(RNT), rargs, 0, g->stream));
+  } else if (mode == MODE_PP && d.warm && d.lazy && g->reach) {
+    // DYN_PP warm start: batch + warm discharge iteration (k_solve), the universal
+    // certificate (k_reach<true>), and -- only if it failed, decided on the device --
+    // the full Alg.8 stage 1 / P / stage 2 (k_solve MODE_PP_CONT, a no-op otherwise)
+    d.split = 1;
+    CK(cudaLaunchCooperativeKernel((const void *)k_solve<NT>, dim3(g->grid_blocks), dim3(NT), args, 0, g->stream));
+    void *rargs[] = {&d};
+    CK(cudaLaunchCooperativeKernel((const void *)k_reach<true>, dim3(g->reach_blocks), dim3(RNT), rargs, 0, g->stream));
+    int32_t mc = MODE_PP_CONT;
+    void *cargs[] = {&d, &mc};
+    CK(cudaLaunchCooperativeKernel((const void *)k_solve<NT>, dim3(g->grid_blocks), dim3(NT), cargs, 0, g->stream));
+    g->launches += 2;
   } else {
     CK(cudaLaunchCooperativeKernel((const void *)k_solve<NT>, dim3(g->grid_blocks), dim3(NT), args, 0, g->stream));
   }
@@ -712,7 +725,10 @@ int dmf_create(int32_t n, const int64_t *row_ptr, const int32_t *col, const int3
   if (g->opt.grid_blocks > 0 && g->opt.grid_blocks < g->grid_blocks) g->grid_blocks = g->opt.grid_blocks;
   {
     int rper = 0;
-    CKB(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&rper, k_reach, RNT, 0));
+    int rper2 = 0;
+    CKB(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&rper, k_reach<false>, RNT, 0));
+    CKB(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&rper2, k_reach<true>, RNT, 0));
+    rper = rper2 < rper ? rper2 : rper;
     if (rper < 1) { fail(DMF_ECUDA, "reach kernel cannot be resident (occupancy 0)"); return bail(DMF_ECUDA); }
     g->reach_blocks = rper * sms;
     if (const char *rc = getenv("DMF_REACH")) g->reach = atoi(rc) != 0;

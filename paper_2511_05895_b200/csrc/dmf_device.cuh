@@ -41,6 +41,8 @@ enum Mode : int32_t {
   MODE_MINCUT = 3,   // forward reach of {s} u Exc  (S_min)
   MODE_MAXCUT = 4,   // complement of backward reach of {t} u Def (S_max)
   MODE_FLOW = 5,     // stage (ii): pseudoflow -> true maximum flow (excess back to s, deficits from t)
+  MODE_PP_CONT = 6,  // DYN_PP after a failed k_reach certificate: full Alg.8 stage 1 from fresh
+                     // labels, P, stage 2, S_min (exits at once when the certificate held)
 };
 
 enum Stat : int {
@@ -93,6 +95,7 @@ struct Ctl {
   int32_t rbq[3];               // bottom-up: rows queued for the warp pass
   unsigned long long rfs[3];    // slots of the level's vertices
   unsigned long long rmu;       // slots of the vertices not labelled at level 0
+  int32_t rfail;                // k_reach certificate: an excess vertex is labelled / s reaches a label
 };
 
 // Everything a kernel needs, passed by value.  Slot arrays are SoA int32[S]:
@@ -144,6 +147,8 @@ struct Dev {
   int32_t imm_act;           // async discharge: activate a pushed head at the push (returning atomic) instead of after the item
   int32_t dmaxch;            // discharge: at most this many chunk items per big-vertex activation (0: CH-slot chunks)
   int32_t scan2;             // chunked discharge: two-pass scan (list admissible slots, one claim, push)
+  int32_t split;             // DYN_PP warm start: the certificate runs in k_reach (the PP launch stops
+                             // after the warm iteration; MODE_PP_CONT continues if it fails)
   int32_t lazy;              // DYN_PP warm start: certify with the universal backward BFS (no pull BFS / stage 2)
   int32_t *plist;            // region P of push-pull stage 2
   int32_t *stamp;            // per-slot batch stamp (duplicate detection)

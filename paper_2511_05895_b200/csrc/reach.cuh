@@ -53,6 +53,7 @@ struct RSm {
   long long it[RSTG];                       // staged frontier items
   int32_t q[RQSTG];                         // staged bottom-up warp-pass candidates
   int32_t icnt, qcnt, ibase, qbase;
+  int32_t hist[2 * GAPW];                   // certificate epilogue: per-CTA label histogram
 };
 
 __device__ __forceinline__ long long r_bsum(RSm &sm, long long x) {
@@ -147,6 +148,7 @@ __device__ __forceinline__ void r_flush(RSm &sm, long long *list, int32_t *cnt, 
   __syncthreads();
 }
 
+template <bool BACK>
 __global__ void __launch_bounds__(RNT, RMINB) k_reach(const __grid_constant__ Dev d) {
   cg::grid_group grid = cg::this_grid();
   __shared__ RSm sm;
@@ -156,10 +158,17 @@ __global__ void __launch_bounds__(RNT, RMINB) k_reach(const __grid_constant__ De
   const int32_t nt = gridDim.x * RNT;
   const int32_t gw = (int32_t)((threadIdx.x >> 5) * gridDim.x + blockIdx.x), nw = gridDim.x * RWPB;
   const bool want_hist = d.local_gap && d.cnt_next;
+  // forward (S_min): labels h-, roots {s} u Exc, t never labelled, a top-down scan reads
+  // c_f(u,v) = res of u's slot; backward (certificate): labels h+, roots {t} u Def, s never
+  // labelled, the residual read is the mirror (c_f(v,u) of u's slot (u,v) = rres)
+  int32_t *const H = BACK ? d.hp : d.hm;
+  const int32_t *const RTD = BACK ? d.rres : d.res;    // top-down: frontier u's slot (u,v) -> v
+  const int32_t *const RBU = BACK ? d.res : d.rres;    // bottom-up: v's slot (v,u), u in the frontier
+  const int32_t xv = BACK ? d.s : d.t;                 // never labelled
   if (threadIdx.x == 0) { sm.tclk = gtimer(); sm.icnt = 0; sm.qcnt = 0; }
   __syncthreads();
   if (blockIdx.x == 0 && want_hist)
-    for (int i = threadIdx.x; i < GAPW; i += RNT) { d.cnt_next[i] = d.cnt[i]; d.cnt_next[GAPW + i] = 0; }
+    for (int i = threadIdx.x; i < GAPW; i += RNT) { d.cnt_next[i] = BACK ? 0 : d.cnt[i]; d.cnt_next[GAPW + i] = 0; }
 
   // ---- roots: level 0 = {s} u {v != t : e(v) > 0}; everything else |V|
   {
@@ -177,10 +186,10 @@ __global__ void __launch_bounds__(RNT, RMINB) k_reach(const __grid_constant__ De
 #pragma unroll
       for (int j = 0; j < 4; j++) {
         const int32_t v = t0 + j * RNT + threadIdx.x;
-        const bool root = v < n && (v == d.s || (v != d.t && ev[j] > 0));
-        if (v < n) d.hm[v] = root ? 0 : n;
+        const bool root = v < n && (BACK ? (v == d.t || (v != d.s && ev[j] < 0)) : (v == d.s || (v != d.t && ev[j] > 0)));
+        if (v < n) H[v] = root ? 0 : n;
         if (root) { fdeg += dg[j]; nroot++; }
-        else if (v < n && v != d.t) udeg += dg[j];
+        else if (v < n && v != xv) udeg += dg[j];
         r_append(sm, d.cq0, &ctl->rcnt[0], root, rb[j], dg[j]);
       }
     }
@@ -210,7 +219,7 @@ __global__ void __launch_bounds__(RNT, RMINB) k_reach(const __grid_constant__ De
     if (L > 0) mu = mu > f ? mu - f : 0;
     if (blockIdx.x == 0 && threadIdx.x == 0) {    // slot nn was last read in level L-1
       ctl->rcnt[nn] = 0; ctl->rfs[nn] = 0; ctl->rnv[nn] = 0; ctl->rbq[nn] = 0;
-      if (want_hist && L < GAPW) d.cnt_next[GAPW + L] = nv;
+      if (!BACK && want_hist && L < GAPW) d.cnt_next[GAPW + L] = nv;
       ctl->stat[ST_LEVELS] += 1;
       ctl->stat[ST_BFS_V] += (unsigned long long)nv;
     }
@@ -224,7 +233,7 @@ __global__ void __launch_bounds__(RNT, RMINB) k_reach(const __grid_constant__ De
 #pragma unroll
         for (int j = 0; j < 4; j++) {
           const int32_t v = t0 + j * RNT + threadIdx.x;
-          h[j] = v < n ? ldv(d.hm + v) : n;
+          h[j] = v < n ? ldv(H + v) : n;
         }
 #pragma unroll
         for (int j = 0; j < 4; j++) {
@@ -257,13 +266,13 @@ __global__ void __launch_bounds__(RNT, RMINB) k_reach(const __grid_constant__ De
 #pragma unroll
             for (int j = 0; j < 8; j++) {
               const int32_t i = b + j * 32 + lane;
-              r[j] = i < end ? ldv(d.res + i) : 0;
+              r[j] = i < end ? ldv(RTD + i) : 0;
               w[j] = i < end ? d.dst[i] : 0;
             }
 #pragma unroll
-            for (int j = 0; j < 8; j++) r[j] = r[j] > 0 && w[j] != d.t && ldl1(d.hm + w[j]) == n;
+            for (int j = 0; j < 8; j++) r[j] = r[j] > 0 && w[j] != xv && ldl1(H + w[j]) == n;
 #pragma unroll
-            for (int j = 0; j < 8; j++) if (r[j]) d.hm[w[j]] = L + 1;
+            for (int j = 0; j < 8; j++) if (r[j]) H[w[j]] = L + 1;
           }
         }
       }
@@ -277,24 +286,20 @@ __global__ void __launch_bounds__(RNT, RMINB) k_reach(const __grid_constant__ De
 #pragma unroll
           for (int j = 0; j < 4; j++) {
             const int32_t i = b + j * 32 + lane;
-            r[j] = i < end ? ldv(d.res + i) : 0;
+            r[j] = i < end ? ldv(RTD + i) : 0;
             w[j] = i < end ? d.dst[i] : 0;
           }
 #pragma unroll
-          for (int j = 0; j < 4; j++)          // stale |V| is harmless: the CAS / the sweep decides
-            r[j] = (r[j] > 0 && w[j] != d.t && ldl1(d.hm + w[j]) == n) ? 1 : 0;
-          if (dense) {
+          for (int j = 0; j < 4; j++)          // stale |V| is harmless: the CAS decides
+            r[j] = (r[j] > 0 && w[j] != xv && ldl1(H + w[j]) == n) ? 1 : 0;
 #pragma unroll
-            for (int j = 0; j < 4; j++) if (r[j]) d.hm[w[j]] = L + 1;
-            continue;
-          }
-#pragma unroll
-          for (int j = 0; j < 4; j++) r[j] = r[j] && atomicCAS(d.hm + w[j], n, L + 1) == n;
+          for (int j = 0; j < 4; j++) r[j] = r[j] && atomicCAS(H + w[j], n, L + 1) == n;
           int32_t rb[4], dg[4];
 #pragma unroll
           for (int j = 0; j < 4; j++) {
             rb[j] = r[j] ? d.row[w[j]] : 0;
             dg[j] = r[j] ? d.row[w[j] + 1] - rb[j] : 0;
+            if (BACK && r[j] && ldv(d.e + w[j]) > 0) ctl->rfail = 1;   // an excess vertex reaches a sink
           }
 #pragma unroll
           for (int j = 0; j < 4; j++) {
@@ -312,13 +317,14 @@ __global__ void __launch_bounds__(RNT, RMINB) k_reach(const __grid_constant__ De
 #pragma unroll
           for (int j = 0; j < 4; j++) {
             const int32_t v = t0 + j * RNT + threadIdx.x;
-            h[j] = v < n ? ldv(d.hm + v) : n;
+            h[j] = v < n ? ldv(H + v) : n;
           }
 #pragma unroll
           for (int j = 0; j < 4; j++) {
             const int32_t v = t0 + j * RNT + threadIdx.x;
             rb[j] = h[j] == L + 1 ? d.row[v] : 0;
             dg[j] = h[j] == L + 1 ? d.row[v + 1] - rb[j] : 0;
+            if (BACK && h[j] == L + 1 && ldv(d.e + v) > 0) ctl->rfail = 1;
           }
 #pragma unroll
           for (int j = 0; j < 4; j++)
@@ -330,17 +336,17 @@ __global__ void __launch_bounds__(RNT, RMINB) k_reach(const __grid_constant__ De
       // ---- bottom-up pass A: thread per unvisited vertex with a short row
       // (the next vertex's label and row bounds are loaded one iteration ahead)
       int32_t v = blockIdx.x * RNT + threadIdx.x;
-      int32_t hN = v < n ? ldv(d.hm + v) : 0, rbN = v < n ? d.row[v] : 0, reN = v < n ? d.row[v + 1] : 0;
+      int32_t hN = v < n ? ldv(H + v) : 0, rbN = v < n ? d.row[v] : 0, reN = v < n ? d.row[v + 1] : 0;
       for (; v - (int32_t)threadIdx.x < n; v += nt) {
         const bool in = v < n;
         const int32_t h = hN, rb = rbN, re = reN;
         {
           const int32_t vn = v + nt;
-          hN = vn < n ? ldv(d.hm + vn) : 0;
+          hN = vn < n ? ldv(H + vn) : 0;
           rbN = vn < n ? d.row[vn] : 0;
           reN = vn < n ? d.row[vn + 1] : 0;
         }
-        const bool cand = in && h == n && v != d.t;
+        const bool cand = in && h == n && v != xv;
         const bool big = cand && re - rb > RBU_T;
         bool found = false;
         if (cand && !big) {
@@ -348,13 +354,16 @@ __global__ void __launch_bounds__(RNT, RMINB) k_reach(const __grid_constant__ De
             int32_t r[4], w[4];
 #pragma unroll
             for (int j = 0; j < 4; j++) {      // in-slot (v,u): rres = c_f(u,v)
-              r[j] = i0 + j < re ? ldv(d.rres + i0 + j) : 0;
+              r[j] = i0 + j < re ? ldv(RBU + i0 + j) : 0;
               w[j] = i0 + j < re ? d.dst[i0 + j] : 0;
             }
 #pragma unroll
-            for (int j = 0; j < 4; j++) found |= r[j] > 0 && ldl1(d.hm + w[j]) == L;   // level-L labels are frozen
+            for (int j = 0; j < 4; j++) found |= r[j] > 0 && ldl1(H + w[j]) == L;   // level-L labels are frozen
           }
-          if (found) { d.hm[v] = L + 1; fdeg += re - rb; nlab++; }
+          if (found) {
+            H[v] = L + 1; fdeg += re - rb; nlab++;
+            if (BACK && ldv(d.e + v) > 0) ctl->rfail = 1;
+          }
         }
         r_queue(sm, d.bul, &ctl->rbq[cur], big, v);
       }
@@ -371,15 +380,18 @@ __global__ void __launch_bounds__(RNT, RMINB) k_reach(const __grid_constant__ De
 #pragma unroll
           for (int j = 0; j < 4; j++) {
             const int32_t i = b + j * 32 + lane;
-            r[j] = i < re ? ldv(d.rres + i) : 0;
+            r[j] = i < re ? ldv(RBU + i) : 0;
             w[j] = i < re ? d.dst[i] : 0;
           }
           bool hit = false;
 #pragma unroll
-          for (int j = 0; j < 4; j++) hit |= r[j] > 0 && ldl1(d.hm + w[j]) == L;
+          for (int j = 0; j < 4; j++) hit |= r[j] > 0 && ldl1(H + w[j]) == L;
           if (__any_sync(0xffffffffu, hit)) { found = true; break; }
         }
-        if (found && lane == 0) { d.hm[v] = L + 1; fdeg += re - rb; nlab++; }
+        if (found && lane == 0) {
+          H[v] = L + 1; fdeg += re - rb; nlab++;
+          if (BACK && ldv(d.e + v) > 0) ctl->rfail = 1;
+        }
       }
     }
     r_flush(sm, nl, &ctl->rcnt[nx], d.bul, &ctl->rbq[cur]);
@@ -393,18 +405,76 @@ __global__ void __launch_bounds__(RNT, RMINB) k_reach(const __grid_constant__ De
     r_lap(d, sm, dense ? ST_T_BFS_CMP : ST_T_BFS, L, nv, (bu ? 2 : 0) | (dense ? 4 : 0) | (cnt << 3));
   }
 
-  // ---- the S_min mask
-  for (int32_t t0 = blockIdx.x * RNT * 4; t0 < n; t0 += nt * 4) {
-    int32_t h[4];
-#pragma unroll
-    for (int j = 0; j < 4; j++) {
-      const int32_t v = t0 + j * RNT + threadIdx.x;
-      h[j] = v < n ? ldv(d.hm + v) : n;
+  if (BACK) {
+    // ---- the certificate (R9): no excess vertex was labelled (checked at labelling) and
+    //      s reaches no labelled vertex (DYN_PP does not re-saturate s, R16)
+    const int32_t sb = d.row[d.s], se = d.row[d.s + 1];
+    bool hit = false;
+    for (int32_t i = sb + blockIdx.x * RNT + (int32_t)threadIdx.x; i < se; i += nt)
+      hit |= ldv(d.res + i) > 0 && ldv(d.hp + d.dst[i]) < n;
+    if (hit) ctl->rfail = 1;
+    grid.sync();
+    if (ldv(&ctl->rfail)) { r_lap(d, sm, ST_T_EPI); return; }   // MODE_PP_CONT takes over
+    // ---- converged: partition = the certificate's reach (T' = labelled, R15), region
+    //      encoding of the next warm start, F (R8), the final labels' histogram
+    long long f = 0;
+    if (want_hist) {
+      for (int i = threadIdx.x; i < 2 * GAPW; i += RNT) sm.hist[i] = 0;
+      __syncthreads();
     }
+    for (int32_t t0 = blockIdx.x * RNT * 2; t0 < n; t0 += nt * 2) {
+      long long ev[2];
+      int32_t hp[2], hm[2];
 #pragma unroll
-    for (int j = 0; j < 4; j++) {
-      const int32_t v = t0 + j * RNT + threadIdx.x;
-      if (v < n) d.mask[v] = h[j] < n ? 1 : 0;
+      for (int j = 0; j < 2; j++) {
+        const int32_t v = t0 + j * RNT + threadIdx.x;
+        ev[j] = v < n ? ldv(d.e + v) : 0;
+        hp[j] = v < n ? ldv(d.hp + v) : n;
+        hm[j] = v < n ? ldv(d.hm + v) : n;
+      }
+#pragma unroll
+      for (int j = 0; j < 2; j++) {
+        const int32_t v = t0 + j * RNT + threadIdx.x;
+        const bool ok = v < n;
+        int32_t hmv = hm[j];
+        if (ok) {
+          f += v == d.t ? ev[j] : (v != d.s && ev[j] < 0 ? ev[j] : 0);
+          const bool tside = hp[j] < n;
+          d.part[v] = tside ? PART_T : PART_S;
+          if (tside) { d.hm[v] = n + 1; hmv = n + 1; }
+          else {
+            d.hp[v] = n + 1;
+            if (hmv > n) { d.hm[v] = n; hmv = n; }
+          }
+        }
+        if (want_hist) {
+          hist_add(sm.hist, ok && hp[j] < n && hp[j] < GAPW, hp[j]);
+          hist_add(sm.hist + GAPW, ok && hmv < n && hmv < GAPW, hmv);
+        }
+      }
+    }
+    if (want_hist) {                               // one global add per non-zero bin per CTA
+      __syncthreads();
+      for (int i = threadIdx.x; i < 2 * GAPW; i += RNT)
+        if (sm.hist[i]) atomicAdd(d.cnt_next + i, sm.hist[i]);
+    }
+    f = r_bsum(sm, f);
+    if (threadIdx.x == 0 && f) atomicAdd(reinterpret_cast<unsigned long long *>(&ctl->flow), (unsigned long long)f);
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctl->lazy_ok = 1;
+  } else {
+    // ---- the S_min mask
+    for (int32_t t0 = blockIdx.x * RNT * 4; t0 < n; t0 += nt * 4) {
+      int32_t h[4];
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        const int32_t v = t0 + j * RNT + threadIdx.x;
+        h[j] = v < n ? ldv(d.hm + v) : n;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        const int32_t v = t0 + j * RNT + threadIdx.x;
+        if (v < n) d.mask[v] = h[j] < n ? 1 : 0;
+      }
     }
   }
   r_lap(d, sm, ST_T_EPI);

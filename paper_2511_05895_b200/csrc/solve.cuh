@@ -1873,6 +1873,7 @@ __device__ int device_loop(const Dev &d, cg::grid_group &grid, Smem &sm, PhaseCl
   const int32_t nt = gridDim.x * NT;
   const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
   for (int iter = 0;; ++iter) {
+   if (lazy && iter >= 1 && d.split) return 2;   // the certificate runs in k_reach<true> (reach.cuh)
    const bool certify = lazy && iter >= 1;       // the universal certificate pass
    const int kind = certify ? (int)RK_PUSH : kind0;
    const bool use0 = kind != RK_MINCUT && kind != RK_MINCUT_P && kind != RK_FILL_T;
@@ -2281,6 +2282,8 @@ template <int NTHREADS>
 __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(const __grid_constant__ Dev d, int32_t mode) {
   cg::grid_group grid = cg::this_grid();
   __shared__ Smem sm;
+  // the continuation of a DYN_PP whose k_reach certificate held has nothing to do
+  if (mode == MODE_PP_CONT && *(const volatile int32_t *)&d.ctl->lazy_ok) return;
   for (int i = threadIdx.x; i < ST_N; i += NTHREADS) sm.stat[i] = 0;
   if (threadIdx.x < 6) sm.st.cnt[threadIdx.x] = 0;
   if (threadIdx.x == 0) { sm.work = 0; sm.tprev = gtimer(); sm.acnt = 0; sm.rcnt = 0; sm.ccnt = 0; sm.astop = 0; sm.apoll = 0;
@@ -2291,7 +2294,8 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(const __grid_con
     // (the final labels' histogram, see the PP epilogue); every other call rebuilds
     // them from its first RESET.  Published by the first grid barrier.
     if (!(mode == MODE_PP && d.warm)) for (int i = threadIdx.x; i < 2 * GAPW; i += NTHREADS) d.cnt[i] = 0;
-    if (mode == MODE_PP || mode == MODE_MINCUT) for (int i = threadIdx.x; i < 2 * GAPW; i += NTHREADS) d.cnt_next[i] = 0;
+    if (mode == MODE_PP || mode == MODE_PP_CONT || mode == MODE_MINCUT)
+      for (int i = threadIdx.x; i < 2 * GAPW; i += NTHREADS) d.cnt_next[i] = 0;
   }
   __syncthreads();
   const int32_t n = d.n;
@@ -2523,15 +2527,20 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(const __grid_con
                });
     f = bg.sum(f);
     if (threadIdx.x == 0 && f) atomicAdd(reinterpret_cast<unsigned long long *>(&ctl->flow), (unsigned long long)f);
-  } else if (mode == MODE_PP) {
+  } else if (mode == MODE_PP || mode == MODE_PP_CONT) {
     // ---- stage 1: push on T || pull on S (Alg.8 l.15-28)
     clk.lap(d, sm, ST_T_PRO);
     // Warm start: discharge on the previous labels, then the universal certificate
     // (R9).  When it holds, the state is converged and Alg.8's remaining work (the
     // two-track BFS, P, stage 2) has nothing to change; the partition is the
     // certificate's reach (R15) and S_min is left to dmf_min_cut_source_side.
-    const int lz = (d.warm && d.lazy) ? device_loop(d, grid, sm, clk, RK_PP, true, false, true, true) : 0;
-    if (lz == 1) {
+    // With d.split the certificate runs in k_reach<true> (lz = 2: nothing more here) and a
+    // MODE_PP_CONT launch continues below (lz = -1) only if it failed.
+    const int lz = mode == MODE_PP_CONT ? -1
+                 : (d.warm && d.lazy) ? device_loop(d, grid, sm, clk, RK_PP, true, false, true, true) : 0;
+    if (lz == 2) {
+      // (handed to k_reach<true>)
+    } else if (lz == 1) {
       long long f = 0;
       int32_t *hist = sm.cand;
       const bool want_hist = d.local_gap && d.cnt_next;
