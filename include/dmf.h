@@ -113,6 +113,8 @@ typedef struct {
                                {t} u {deficient vertices} reaches no excess vertex and s reaches none of
                                its labels); when it holds the call ends there (partition = that BFS's
                                reach, R15) and S_min is computed by dmf_min_cut_source_side on demand.
+                               The certificate runs in k_reach; a failed one hands over to a second
+                               k_solve launch (decided on the device, no host round trip).
                                0 => on, < 0 => off (always the full Alg.8 stage 1 / P / stage 2) [DMF_CERTIFY] */
     int32_t reserved[7];    /* must be zero */
 } dmf_options;
@@ -209,7 +211,10 @@ int dmf_flow_value(const dmf_graph *g, int64_t *out);
 
 /* Minimal min-cut source side S_min (unique): mask[v] = 1 iff v is reachable in the
  * residual graph from {s} u {v not in {s,t} : e(v) > 0} (reading R19; equals
- * the residual reach of s for any true maximum flow).  mask: uint8[n], host or device. */
+ * the residual reach of s for any true maximum flow).  mask: uint8[n], host or device.
+ * Cached when the last DYN_PP computed it (the full stage-1 path); otherwise one launch
+ * of the dedicated BFS kernel k_reach (csrc/reach.cuh), which also refreshes h- with the
+ * exact forward distances used by the next DYN_PP warm start. */
 int dmf_min_cut_source_side(dmf_graph *g, uint8_t *mask);
 
 /* Maximal min-cut source side S_max: mask[v] = 1 iff v cannot reach {t} u {deficient}
