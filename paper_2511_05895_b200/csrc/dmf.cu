@@ -102,6 +102,8 @@ struct dmf_graph {
   int32_t *ddbg = nullptr;   // device view
   int grid_blocks = 0;
   int reach_blocks = 0;      // cooperative grid of k_reach (S_min query)
+  int32_t cert_skip = 0;     // DYN_PP calls left that skip the certificate (after a failed one)
+  int32_t cert_backoff = 0;  // current back-off length: 0, 1, 3, 7, 15, 16
   bool reach = true;         // DMF_REACH=0: the S_min query runs k_solve's MINCUT mode and the DYN_PP
                              // certificate runs inside k_solve instead of k_reach
   double watchdog_s = 0;
@@ -361,10 +363,18 @@ static int run_solve(dmf_graph *g, int32_t mode, const Dev &dv) {
   d.async = (mode == MODE_STATIC ? g->async_static : g->async) ? 1 : 0;
   int32_t md = mode;
   void *args[] = {&d, &md};
+  bool attempted = false;           // a certificate attempt (k_reach<true>) was made
   if (mode == MODE_MINCUT && g->reach) {
     void *rargs[] = {&d};
     CK(cudaLaunchCooperativeKernel((const void *)k_reach<false>, dim3(g->reach_blocks), dim3(RNT), rargs, 0, g->stream));
+  } else if (mode == MODE_PP && d.warm && d.lazy && g->cert_skip > 0) {
+    // the last certificate attempt failed: run the full stage 1 from the warm labels
+    // for a while (exponential back-off), without the certificate's extra BFS
+    g->cert_skip--;
+    d.lazy = 0;
+    CK(cudaLaunchCooperativeKernel((const void *)k_solve<NT>, dim3(g->grid_blocks), dim3(NT), args, 0, g->stream));
   } else if (mode == MODE_PP && d.warm && d.lazy && g->reach) {
+    attempted = true;
     // DYN_PP warm start: batch + warm discharge iteration (k_solve), the universal
     // certificate (k_reach<true>), and -- only if it failed, decided on the device --
     // the full Alg.8 stage 1 / P / stage 2 (k_solve MODE_PP_CONT, a no-op otherwise)
@@ -432,6 +442,10 @@ static int run_solve(dmf_graph *g, int32_t mode, const Dev &dv) {
   st.tail_stops = (int64_t)c.stat[ST_TAIL_STOPS];
   st.stage2_skipped = (int64_t)c.stat[ST_S2_SKIP];
   st.certified = c.lazy_ok;
+  if (attempted && c.status == 0) {     // back-off of the certificate after a failed attempt
+    g->cert_backoff = c.lazy_ok ? 0 : (g->cert_backoff * 2 + 1 < 16 ? g->cert_backoff * 2 + 1 : 16);
+    g->cert_skip = g->cert_backoff;
+  }
   st.batch_entries = dv.k;
   st.device_ms = ms;
   if (c.pad != 0) fprintf(stderr, "[dmf debug] vertex %d discharged concurrently\n", c.pad - 1);

@@ -214,6 +214,7 @@ __global__ void __launch_bounds__(RNT, RMINB) k_reach(const __grid_constant__ De
     const int cur = L % 3, nx = (L + 1) % 3, nn = (L + 2) % 3;
     const int32_t nv = ldv(&ctl->rnv[cur]);
     if (nv == 0) break;                            // nothing labelled at level L: done
+    if (BACK && ldv(&ctl->rfail)) break;           // certificate already refuted: stop here
     int32_t cnt = ldv(&ctl->rcnt[cur]);
     const unsigned long long f = (unsigned long long)ldv(reinterpret_cast<const long long *>(&ctl->rfs[cur]));
     if (L > 0) mu = mu > f ? mu - f : 0;

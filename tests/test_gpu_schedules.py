@@ -280,14 +280,15 @@ def test_device_buffers_on_the_default_stream(dmf):
 def test_certificate_both_outcomes(dmf):
     """DYN_PP warm start: the k_reach certificate holds on small batches (the PP launch
     ends there) and fails when a tiny work budget leaves excess after the warm iteration
-    (the MODE_PP_CONT launch runs the full Alg.8 stage 1); both outcomes are exact."""
+    (the MODE_PP_CONT launch runs the full Alg.8 stage 1; later calls then skip the
+    certificate for a back-off period); every outcome is exact."""
     g = W.rmat(15, 16, 1, 7)
     for knobs, want in ((dict(), 1), (dict(schedule="async", budget_mul=-1000000, tail_items=1), 0)):
         f = dmf.DynMaxFlow.from_graph(g, **knobs)
         f.static_solve()
         st = W.CapState(g)
         seen = set()
-        for j, frac in enumerate([0.001, 0.01, 0.001, 0.01]):
+        for j, frac in enumerate([0.001, 0.01, 0.001, 0.01, 0.001, 0.001]):
             b = W.rmat_batch(g, st, frac, 700 + j)
             st.apply(b)
             f.apply_batch(b.u, b.v, b.new_cap, algo="pp")

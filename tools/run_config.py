@@ -38,7 +38,9 @@ for j in range(nb):
     else:
         b = W.rmat_batch(g, st, frac, 100 + j)
     st.apply(b)
-    F = f.apply_batch(b.u, b.v, b.new_cap, algo=algo); show(f"{algo} b{j} k={b.k}", F); check(st.graph(), F)
+    F = f.apply_batch(b.u, b.v, b.new_cap, algo=algo); show(f"{algo} b{j} k={b.k}", F)
+    f.min_cut_source_side(); print(f"    cut query {f.stats()['query_ms']:.3f} ms certified={f.stats()['certified']}", flush=True)
+    check(st.graph(), F)
 F = f.static_solve(); show("re-static", F)
 F = f.static_solve_pp(); show("re-static-pp", F)
 F = f.to_flow(); show("to_flow", F)
