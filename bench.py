@@ -77,6 +77,13 @@ def algorithmic_bytes(st: dict, n: int) -> int:
                + st["batch_entries"] * B_BATCH_ENTRY + st["reset_vertices"] * B_RESET_VERTEX + n * 9)
 
 
+def cut_algorithmic_bytes(bfs_v: int, bfs_slots: int, n: int) -> int:
+    """Bytes of one S_min query (k_reach<false>): root sweep (e read + label write, 12 B
+    per vertex), BFS (12 B per labelled vertex, 8 B per scanned slot), mask sweep (label
+    read + mask write, 5 B per vertex)."""
+    return int(n * 12 + bfs_v * B_BFS_VERTEX + bfs_slots * B_BFS_SLOT + n * 5)
+
+
 def phase_roofline(per: list, peak: float) -> dict:
     """Per-step achieved algorithmic GB/s of the three method steps the north star names,
     from the in-kernel phase clock (one persistent kernel: ncu cannot split its phases):
@@ -182,7 +189,7 @@ def run_snapshot(P, torch, dev, spec, W_, K, algo, no_cut=False):
     fa.static_solve()
     out["F_static_initial"] = fa.flow_value()
     raw = [P.Stats() for _ in batches]
-    qms = []
+    qms, qalg = [], []
     for j in range(W_):
         u, v, c = dbat[j]
         fa.apply_batch(u, v, c, algo=algo)
@@ -199,7 +206,9 @@ def run_snapshot(P, torch, dev, spec, W_, K, algo, no_cut=False):
         fa.raw_stats(raw[j])
         if not no_cut:
             fa.min_cut_source_side(dmask)
-            qms.append(fa.raw_stats().query_ms)
+            rq = fa.raw_stats()
+            qms.append(rq.query_ms)
+            qalg.append(cut_algorithmic_bytes(rq.query_bfs_vertices, rq.query_bfs_slots, g.n))
         ev[i + 1].record(stream)
     torch.cuda.synchronize()
     out["elapsed_ms"] = ev[0].elapsed_time(ev[K])
@@ -207,6 +216,7 @@ def run_snapshot(P, torch, dev, spec, W_, K, algo, no_cut=False):
     out["launches"] = fa.stats()["kernel_launches"] - launches0
     out["per"] = [P.DynMaxFlow.stats_to_dict(raw[j]) for j in range(W_, W_ + K)]
     out["query_ms"] = qms
+    out["query_alg_bytes"] = qalg
     out["F_final"] = fa.flow_value()
     out["k_timed"] = int(sum(batches[j].k for j in range(W_, W_ + K)))
     fa.close()
@@ -279,7 +289,16 @@ def summarize(snaps, K, peak):
     if qms and scut:
         with_cut = (float(np.median(static_ms)) + float(np.median(scut))) / \
                    (float(np.median(batch_ms)) + float(np.median(qms)))
+    qab = [x for s in snaps for x in s.get("query_alg_bytes", [])]
+    cut_roof = None
+    if qms and qab:
+        cm = float(np.mean(qms))
+        ca = float(np.mean(qab))
+        cut_roof = {"kernel": "k_reach<false> (S_min query)", "bound": "hbm", "achieved": ca / (cm * 1e-3) / 1e9,
+                    "peak": peak, "unit": "GB/s", "frac": ca / (cm * 1e-3) / 1e9 / peak,
+                    "algorithmic_bytes_per_launch": ca, "kernel_ms": cm}
     return {
+        "cut_roofline": cut_roof,
         "cut_query_ms": {"p50": pctl(qms, 50), "p90": pctl(qms, 90),
                          "static_p50": pctl(scut, 50)} if qms else None,
         "speedup_vs_static_with_cut": with_cut,
@@ -489,11 +508,12 @@ def main():
         if world == 1 and not args.no_cpu_baseline:
             cpu = cpu_baseline(workload_spec(args.workload, Wm, K, frac=args.frac), Wm, K, g0["k"], args.cpu_budget_s)
         roof = summ["roofline"]
-        roof.update({"traffic": traffic, "kernel": f"k_solve (mode {args.algo.upper()} batch launch)",
+        roof.update({"traffic": traffic,
+                     "kernel": f"dmf_apply_batch ({args.algo.upper()}): k_solve + k_reach<true> certificate launches",
                      "peak_source": peak_src,
-                     "traffic_source": "profiles/ncu_traffic.json: ncu dram__bytes_read+write of timed step 0's "
-                                       "k_solve launch at the recorded commit; its algorithmic bytes are recorded "
-                                       "beside it"})
+                     "traffic_source": "profiles/ncu_traffic.json: ncu dram__bytes_read+write summed over timed "
+                                       "step 0's dmf_apply_batch launches at the recorded commit; their "
+                                       "algorithmic bytes are recorded beside it"})
         line = {
             "metric": METRIC, "value": k_all / (el_max * 1e-3), "unit": UNIT, "n_gpus": world, "steps": K,
             "warmup": Wm, "ms_per_step": el_max / (K * len(mine)), "higher_is_better": True, "scaling": "weak",
@@ -512,7 +532,7 @@ def main():
             "static_solve_ms": summ["static_ms"],
             "speedup_vs_static": summ["speedup_vs_static"],
             "speedup_vs_static_with_cut": summ["speedup_vs_static_with_cut"],
-            "cut_query_ms": summ["cut_query_ms"],
+            "cut_query_ms": summ["cut_query_ms"], "cut_roofline": summ["cut_roofline"],
             "speedup_vs_static_per_batch": summ["speedup_vs_static_per_batch"],
             "step_ms": summ["step_ms"], "e2e_step_ms": summ["e2e_step_ms"],
             "edges_per_s": summ["edges_per_s"], "static_edges_per_s": summ["static_edges_per_s"],

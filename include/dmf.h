@@ -156,6 +156,8 @@ typedef struct {
     int64_t certified;         /* DYN_PP: 1 if the warm iteration was certified converged (options.certify) */
     float   query_ms;          /* device time of the last dmf_min_cut_source_side / dmf_max_cut_source_side
                                   launch (0 when S_min was already cached by the last DYN_PP call) */
+    int64_t query_bfs_vertices;/* that query's BFS: vertices labelled and slots scanned */
+    int64_t query_bfs_slots;
 } dmf_stats;
 
 /* Fill *opt with defaults (all zero / NULL; algo = DMF_DYN_PP). */

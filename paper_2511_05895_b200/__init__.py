@@ -61,7 +61,8 @@ class Stats(ctypes.Structure):
                 ("t_bfs_us", ctypes.c_float), ("t_discharge_us", ctypes.c_float), ("t_rie_us", ctypes.c_float),
                 ("t_epilogue_us", ctypes.c_float), ("gap_levels", ctypes.c_int64), ("gap_skips", ctypes.c_int64),
                 ("topology_rounds", ctypes.c_int64), ("tail_stops", ctypes.c_int64), ("stage2_skipped", ctypes.c_int64),
-                ("certified", ctypes.c_int64), ("query_ms", ctypes.c_float)]
+                ("certified", ctypes.c_int64), ("query_ms", ctypes.c_float),
+                ("query_bfs_vertices", ctypes.c_int64), ("query_bfs_slots", ctypes.c_int64)]
 
 
 class DMFError(RuntimeError):

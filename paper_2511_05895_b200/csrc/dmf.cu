@@ -825,10 +825,14 @@ static int cut_query(dmf_graph *g, uint8_t *mask, int32_t mode) {
     Dev d = make_dev(g);
     int rc = run_solve(g, mode, d);
     keep.query_ms = g->stats.device_ms;
+    keep.query_bfs_vertices = g->stats.bfs_vertices;
+    keep.query_bfs_slots = g->stats.bfs_slots;
     g->stats = keep;
     if (rc) return rc;
   } else {
     g->stats.query_ms = 0.f;
+    g->stats.query_bfs_vertices = 0;
+    g->stats.query_bfs_slots = 0;
   }
   CK(cudaMemcpyAsync(mask, g->mask, (size_t)g->n, cudaMemcpyDefault, g->stream));
   CK(cudaStreamSynchronize(g->stream));

@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(RNT, RMINB) k_reach(const __grid_constant__ De
     }
     long long *cl = (L & 1) ? d.cq1 : d.cq0;
     long long *nl = (L & 1) ? d.cq0 : d.cq1;
-    long long fdeg = 0, nlab = 0;
+    long long fdeg = 0, nlab = 0, slots = 0;      // (slots: scanned, for the stats)
     const bool bu = f * RALPHA > mu;
     if (!bu && !built) {                           // the level's items: {v : hm[v] = L}
       for (int32_t t0 = blockIdx.x * RNT * 4; t0 < n; t0 += nt * 4) {
@@ -262,6 +262,7 @@ __global__ void __launch_bounds__(RNT, RMINB) k_reach(const __grid_constant__ De
           const long long it = itn;
           itn = x + nw < cnt ? cl[x + nw] : 0;
           const int32_t beg = (int32_t)(uint32_t)it, end = (int32_t)(it >> 32);
+          if (lane == 0) slots += end - beg;
           for (int32_t b = beg; b < end; b += 256) {
             int32_t r[8], w[8];
 #pragma unroll
@@ -282,6 +283,7 @@ __global__ void __launch_bounds__(RNT, RMINB) k_reach(const __grid_constant__ De
         const long long it = itn;
         itn = x + nw < cnt ? cl[x + nw] : 0;
         const int32_t beg = (int32_t)(uint32_t)it, end = (int32_t)(it >> 32);
+        if (lane == 0) slots += end - beg;
         for (int32_t b = beg; b < end; b += 128) {
           int32_t r[4], w[4];
 #pragma unroll
@@ -352,6 +354,7 @@ __global__ void __launch_bounds__(RNT, RMINB) k_reach(const __grid_constant__ De
         bool found = false;
         if (cand && !big) {
           for (int32_t i0 = rb; i0 < re && !found; i0 += 4) {
+            slots += min(4, re - i0);
             int32_t r[4], w[4];
 #pragma unroll
             for (int j = 0; j < 4; j++) {      // in-slot (v,u): rres = c_f(u,v)
@@ -377,6 +380,7 @@ __global__ void __launch_bounds__(RNT, RMINB) k_reach(const __grid_constant__ De
         const int32_t rb = d.row[v], re = d.row[v + 1];
         bool found = false;
         for (int32_t b = rb; b < re; b += 128) {
+          if (lane == 0) slots += min(128, re - b);
           int32_t r[4], w[4];
 #pragma unroll
           for (int j = 0; j < 4; j++) {
@@ -397,8 +401,9 @@ __global__ void __launch_bounds__(RNT, RMINB) k_reach(const __grid_constant__ De
     }
     r_flush(sm, nl, &ctl->rcnt[nx], d.bul, &ctl->rbq[cur]);
     built = !bu && !dense;
-    fdeg = r_bsum(sm, fdeg); nlab = r_bsum(sm, nlab);
+    fdeg = r_bsum(sm, fdeg); nlab = r_bsum(sm, nlab); slots = r_bsum(sm, slots);
     if (threadIdx.x == 0) {
+      if (slots) atomicAdd(&ctl->stat[ST_BFS_SLOTS], (unsigned long long)slots);
       if (fdeg) atomicAdd(&ctl->rfs[nx], (unsigned long long)fdeg);
       if (nlab) atomicAdd(&ctl->rnv[nx], (int32_t)nlab);
     }
