@@ -171,6 +171,14 @@ def pctl(x, q):
     return float(np.percentile(np.asarray(x, np.float64), q)) if len(x) else None
 
 
+_T0 = time.time()
+
+
+def progress(msg: str) -> None:
+    """Stage marks on stderr (the JSON line stays the only stdout output)."""
+    print(f"[bench {time.time() - _T0:7.1f}s] {msg}", file=sys.stderr, flush=True)
+
+
 def run_snapshot(P, torch, dev, spec, W_, K, algo, no_cut=False):
     """One replica: handles A (device-resident timed steps), B (e2e from host buffers on
     the same batches) and C (static re-solves of the same capacity snapshots)."""
@@ -184,6 +192,7 @@ def run_snapshot(P, torch, dev, spec, W_, K, algo, no_cut=False):
     hmask = torch.empty(g.n, dtype=torch.uint8).pin_memory()
     torch.cuda.synchronize()
 
+    progress(f"snapshot {spec.get('scale')} built (n={g.n}); A: device-resident")
     # ---- A: device-resident
     fa = P.DynMaxFlow.from_graph(g, algo=algo)
     fa.static_solve()
@@ -221,6 +230,7 @@ def run_snapshot(P, torch, dev, spec, W_, K, algo, no_cut=False):
     out["k_timed"] = int(sum(batches[j].k for j in range(W_, W_ + K)))
     fa.close()
 
+    progress("B: end to end")
     # ---- B: end to end through the public API, same batches, pinned host buffers
     fb = P.DynMaxFlow.from_graph(g, algo=algo)
     fb.static_solve()
@@ -245,6 +255,7 @@ def run_snapshot(P, torch, dev, spec, W_, K, algo, no_cut=False):
     assert fb.flow_value() == out["F_final"], "e2e handle diverged from the device-resident one"
     fb.close()
 
+    progress("C: static re-solves")
     # ---- C: static re-solve of every timed capacity snapshot (the paper's baseline)
     fc = P.DynMaxFlow.from_graph(g, algo=algo)
     fc.static_solve()
@@ -487,6 +498,7 @@ def main():
         g0 = snaps[0]
         extra = None
         if world == 1 and args.workload == "rmat22" and not args.no_extra:
+            progress("RMAT-20 figures")
             s20 = run_snapshot(P, torch, dev, workload_spec("rmat20", Wm, K, frac=args.frac), Wm, K, args.algo,
                                args.no_cut)
             sm20 = summarize([s20], K, peak)
@@ -506,7 +518,9 @@ def main():
                 traffic = None
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
+            progress("cpu baseline (oracle pool)")
             cpu = cpu_baseline(workload_spec(args.workload, Wm, K, frac=args.frac), Wm, K, g0["k"], args.cpu_budget_s)
+            progress("done")
         roof = summ["roofline"]
         roof.update({"traffic": traffic,
                      "kernel": f"dmf_apply_batch ({args.algo.upper()}): k_solve + k_reach<true> certificate launches",

@@ -90,7 +90,7 @@ struct dmf_graph {
   long long *e = nullptr;
   uint8_t *part = nullptr, *mask = nullptr, *rlf = nullptr;
   int32_t *bbuf = nullptr;   // batch staging: u, v, c, slot, 3 undo records  (7 * bcap)
-  int2 *htab = nullptr;      // (u,v) -> slot table
+  int4 *htab = nullptr;      // (u,v) -> slot table
   int32_t hmask = 0;
   int64_t bcap = 0;
   Ctl *ctl = nullptr;
@@ -208,14 +208,21 @@ __global__ void k_slots(int32_t n, int64_t S, const unsigned long long *ukey, co
   }
 }
 
-// (u,v) -> slot table for O(1) batch lookups (linear probing; entry {v, slot}).
-__global__ void k_hash_insert(int64_t S, int32_t n, const unsigned long long *ukey, int2 *htab, uint32_t hmask) {
+// (u,v) -> slot table for O(1) batch lookups (linear probing; 16-byte entry
+// {u, v, slot, rev[slot]}: one probe gives both slots of the pair, no row lookup).
+// The key half is claimed by a 64-bit CAS, the value half stored after it (the table
+// is read only by later launches).
+__global__ void k_hash_insert(int64_t S, int32_t n, const unsigned long long *ukey, const int32_t *rev, int4 *htab,
+                              uint32_t hmask) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < S; i += (int64_t)gridDim.x * blockDim.x) {
     const unsigned long long k = ukey[i];
     const int32_t u = (int32_t)(k / (unsigned long long)n), v = (int32_t)(k % (unsigned long long)n);
-    const unsigned long long ent = ((unsigned long long)(uint32_t)i << 32) | (uint32_t)v;
+    const unsigned long long key = ((unsigned long long)(uint32_t)v << 32) | (uint32_t)u;   // {x = u, y = v}
     for (uint32_t h = slot_hash(u, v) & hmask;; h = (h + 1) & hmask)
-      if (atomicCAS(reinterpret_cast<unsigned long long *>(htab + h), ~0ull, ent) == ~0ull) break;
+      if (atomicCAS(reinterpret_cast<unsigned long long *>(htab + h), ~0ull, key) == ~0ull) {
+        reinterpret_cast<int2 *>(htab + h)[1] = make_int2((int32_t)i, rev[i]);
+        break;
+      }
   }
 }
 
@@ -697,16 +704,16 @@ int dmf_create(int32_t n, const int64_t *row_ptr, const int32_t *col, const int3
     if (S > (1LL << 30)) { fail(DMF_EOVERFLOW, "too many slots for the slot table (%lld > 2^30)", (long long)S); return bail(DMF_EOVERFLOW); }
     size_t T = 1024;
     while (T < 2 * (size_t)S) T <<= 1;
-    g->htab = (int2 *)g->alloc(T * sizeof(int2));
+    g->htab = (int4 *)g->alloc(T * sizeof(int4));
     if (!g->htab) { fail(DMF_ENOMEM, "device allocation failed (slot table)"); return bail(DMF_ENOMEM); }
     g->hmask = (int32_t)(T - 1);
-    CKB(cudaMemsetAsync(g->htab, 0xff, T * sizeof(int2), st));
+    CKB(cudaMemsetAsync(g->htab, 0xff, T * sizeof(int4), st));
   }
   if (S) {
     CKB(cudaMemsetAsync(err, 0, 64, st));
     k_rows<<<blocks(nn + 1), TB, 0, st>>>(n, S, ukey, g->row);
-    k_hash_insert<<<blocks(S), TB, 0, st>>>(S, n, ukey, g->htab, (uint32_t)g->hmask);
     k_slots<<<blocks(S), TB, 0, st>>>(n, S, ukey, capsum, g->dst, g->rev, g->cap, err);
+    k_hash_insert<<<blocks(S), TB, 0, st>>>(S, n, ukey, g->rev, g->htab, (uint32_t)g->hmask);
     unsigned long long *msum = (unsigned long long *)(err + 8);
     k_sum_i32<<<blocks(S), TB, 0, st>>>(S, isinput, msum);
     CKB(cudaGetLastError());

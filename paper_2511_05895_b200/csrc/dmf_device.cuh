@@ -96,6 +96,7 @@ struct Ctl {
   unsigned long long rfs[3];    // slots of the level's vertices
   unsigned long long rmu;       // slots of the vertices not labelled at level 0
   int32_t rfail;                // k_reach certificate: an excess vertex is labelled / s reaches a label
+  int32_t rfl[3];               // the same, per level % 3 (read at the top of the next level)
 };
 
 // Everything a kernel needs, passed by value.  Slot arrays are SoA int32[S]:
@@ -155,7 +156,7 @@ struct Dev {
   const int32_t *bu, *bv, *bc;  // batch entries
   int32_t *bslot;            // slot of each batch entry
   int32_t *brec;             // per batch entry: residual delta, clamp, S->T saturation (undo of an invalid batch)
-  const int2 *htab;          // (u,v) -> slot table {v, slot}, {-1,-1} empty
+  const int4 *htab;          // (u,v) -> slot table {u, v, slot, rev[slot]}, x = -1 empty
   int32_t hmask;
   uint8_t *mask;             // cut output
   Ctl *ctl;

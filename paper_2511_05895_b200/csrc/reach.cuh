@@ -84,6 +84,16 @@ __device__ __forceinline__ void r_lap(const Dev &d, RSm &sm, int which, int32_t 
   }
 }
 
+// Certificate refuted during level L: the global flag decides after the final barrier;
+// the early exit at the top of level L+1 reads the level's own slot rfl[(L+1) % 3],
+// which no thread writes during level L+1 (a single flag read there would race with
+// writers of level L+1: CTAs would leave the level loop at different levels and
+// their grid barriers would no longer pair up).
+__device__ __forceinline__ void r_refute(Ctl *ctl, int nx) {
+  ctl->rfl[nx] = 1;
+  ctl->rfail = 1;
+}
+
 // warp-convergent: lanes with pred append the row [rb, rb + deg) of a labelled vertex as
 // ceil(deg / RCH) frontier items, each a slot range (end << 32 | begin): a top-down
 // level then needs no row lookup per item.  Items are
@@ -214,12 +224,12 @@ __global__ void __launch_bounds__(RNT, RMINB) k_reach(const __grid_constant__ De
     const int cur = L % 3, nx = (L + 1) % 3, nn = (L + 2) % 3;
     const int32_t nv = ldv(&ctl->rnv[cur]);
     if (nv == 0) break;                            // nothing labelled at level L: done
-    if (BACK && ldv(&ctl->rfail)) break;           // certificate already refuted: stop here
+    if (BACK && ldv(&ctl->rfl[cur])) break;        // certificate refuted at level L-1: stop here
     int32_t cnt = ldv(&ctl->rcnt[cur]);
     const unsigned long long f = (unsigned long long)ldv(reinterpret_cast<const long long *>(&ctl->rfs[cur]));
     if (L > 0) mu = mu > f ? mu - f : 0;
     if (blockIdx.x == 0 && threadIdx.x == 0) {    // slot nn was last read in level L-1
-      ctl->rcnt[nn] = 0; ctl->rfs[nn] = 0; ctl->rnv[nn] = 0; ctl->rbq[nn] = 0;
+      ctl->rcnt[nn] = 0; ctl->rfs[nn] = 0; ctl->rnv[nn] = 0; ctl->rbq[nn] = 0; ctl->rfl[nn] = 0;
       if (!BACK && want_hist && L < GAPW) d.cnt_next[GAPW + L] = nv;
       ctl->stat[ST_LEVELS] += 1;
       ctl->stat[ST_BFS_V] += (unsigned long long)nv;
@@ -302,7 +312,7 @@ __global__ void __launch_bounds__(RNT, RMINB) k_reach(const __grid_constant__ De
           for (int j = 0; j < 4; j++) {
             rb[j] = r[j] ? d.row[w[j]] : 0;
             dg[j] = r[j] ? d.row[w[j] + 1] - rb[j] : 0;
-            if (BACK && r[j] && ldv(d.e + w[j]) > 0) ctl->rfail = 1;   // an excess vertex reaches a sink
+            if (BACK && r[j] && ldv(d.e + w[j]) > 0) r_refute(ctl, nx);   // an excess vertex reaches a sink
           }
 #pragma unroll
           for (int j = 0; j < 4; j++) {
@@ -327,7 +337,7 @@ __global__ void __launch_bounds__(RNT, RMINB) k_reach(const __grid_constant__ De
             const int32_t v = t0 + j * RNT + threadIdx.x;
             rb[j] = h[j] == L + 1 ? d.row[v] : 0;
             dg[j] = h[j] == L + 1 ? d.row[v + 1] - rb[j] : 0;
-            if (BACK && h[j] == L + 1 && ldv(d.e + v) > 0) ctl->rfail = 1;
+            if (BACK && h[j] == L + 1 && ldv(d.e + v) > 0) r_refute(ctl, nx);
           }
 #pragma unroll
           for (int j = 0; j < 4; j++)
@@ -366,7 +376,7 @@ __global__ void __launch_bounds__(RNT, RMINB) k_reach(const __grid_constant__ De
           }
           if (found) {
             H[v] = L + 1; fdeg += re - rb; nlab++;
-            if (BACK && ldv(d.e + v) > 0) ctl->rfail = 1;
+            if (BACK && ldv(d.e + v) > 0) r_refute(ctl, nx);
           }
         }
         r_queue(sm, d.bul, &ctl->rbq[cur], big, v);
@@ -395,7 +405,7 @@ __global__ void __launch_bounds__(RNT, RMINB) k_reach(const __grid_constant__ De
         }
         if (found && lane == 0) {
           H[v] = L + 1; fdeg += re - rb; nlab++;
-          if (BACK && ldv(d.e + v) > 0) ctl->rfail = 1;
+          if (BACK && ldv(d.e + v) > 0) r_refute(ctl, nx);
         }
       }
     }

@@ -2221,10 +2221,9 @@ __device__ __forceinline__ uint32_t slot_hash(int32_t u, int32_t v) {
   return (uint32_t)k;
 }
 __device__ __forceinline__ int32_t find_slot(const Dev &d, int32_t u, int32_t v) {
-  const int32_t lo = d.row[u], hi = d.row[u + 1];
   for (uint32_t h = slot_hash(u, v) & (uint32_t)d.hmask;; h = (h + 1) & (uint32_t)d.hmask) {
-    const int2 e = __ldg(d.htab + h);
-    if (e.x == v && e.y >= lo && e.y < hi) return e.y;
+    const int4 e = __ldg(d.htab + h);
+    if (e.x == u && e.y == v) return e.z;
     if (e.x < 0) return -1;
   }
 }
@@ -2332,52 +2331,49 @@ __global__ void __launch_bounds__(NTHREADS, MIN_BLOCKS) k_solve(const __grid_con
     // first dependent use (the pass is bound by dependent random accesses).
     constexpr int EU = 2;
     for (int64_t j0 = gt; j0 < d.k; j0 += (int64_t)EU * nt) {
-      int32_t u[EU], v[EU], c[EU], lo[EU], hi[EU], i[EU], st[EU], ri[EU], cap0[EU];
+      int32_t u[EU], v[EU], c[EU], i[EU], st[EU], ri[EU], cap0[EU];
       uint8_t pu[EU], pv[EU];
       bool ok[EU];
-      int2 e0[EU];
+      int4 e0[EU];
       uint32_t h0[EU];
 #pragma unroll
-      for (int q = 0; q < EU; q++) {               // entry, row bounds, parts, first probe
+      for (int q = 0; q < EU; q++) {               // entry, parts, first probe
         const int64_t j = j0 + (int64_t)q * nt;
         ok[q] = j < d.k;
         u[q] = ok[q] ? d.bu[j] : 0; v[q] = ok[q] ? d.bv[j] : 0; c[q] = ok[q] ? d.bc[j] : 0;
         if (ok[q] && (u[q] < 0 || u[q] >= n || v[q] < 0 || v[q] >= n)) { set_status(d, -1, (int32_t)j); ok[q] = false; }
         else if (ok[q] && (c[q] < 0 || c[q] > 1073741823)) { set_status(d, -7, (int32_t)j); ok[q] = false; }
-        lo[q] = ok[q] ? d.row[u[q]] : 0; hi[q] = ok[q] ? d.row[u[q] + 1] : 0;
         pu[q] = (ok[q] && mode == MODE_PP) ? ldv(d.part + u[q]) : (uint8_t)0;
         pv[q] = (ok[q] && mode == MODE_PP) ? ldv(d.part + v[q]) : (uint8_t)0;
         h0[q] = ok[q] ? slot_hash(u[q], v[q]) & (uint32_t)d.hmask : 0u;
-        e0[q] = ok[q] ? __ldg(d.htab + h0[q]) : make_int2(-1, -1);
+        e0[q] = ok[q] ? __ldg(d.htab + h0[q]) : make_int4(-1, -1, -1, -1);
       }
 #pragma unroll
-      for (int q = 0; q < EU; q++) {               // resolve the slot (rarely a second probe)
-        i[q] = -1;
+      for (int q = 0; q < EU; q++) {               // resolve slot and reverse slot (rarely a second probe)
+        i[q] = -1; ri[q] = 0;
         if (!ok[q]) continue;
-        if (e0[q].x == v[q] && e0[q].y >= lo[q] && e0[q].y < hi[q]) i[q] = e0[q].y;
+        if (e0[q].x == u[q] && e0[q].y == v[q]) { i[q] = e0[q].z; ri[q] = e0[q].w; }
         else if (e0[q].x >= 0) {
           for (uint32_t h = (h0[q] + 1) & (uint32_t)d.hmask;; h = (h + 1) & (uint32_t)d.hmask) {
-            const int2 e = __ldg(d.htab + h);
-            if (e.x == v[q] && e.y >= lo[q] && e.y < hi[q]) { i[q] = e.y; break; }
+            const int4 e = __ldg(d.htab + h);
+            if (e.x == u[q] && e.y == v[q]) { i[q] = e.z; ri[q] = e.w; break; }
             if (e.x < 0) break;
           }
         }
         if (i[q] < 0) { set_status(d, -2, (int32_t)(j0 + (int64_t)q * nt)); ok[q] = false; }
       }
 #pragma unroll
-      for (int q = 0; q < EU; q++) {               // duplicate stamp, capacity, reverse slot
+      for (int q = 0; q < EU; q++) {               // duplicate stamp; new capacity in, old one out
         const int64_t j = j0 + (int64_t)q * nt;
         if (j < d.k) d.bslot[j] = ok[q] ? i[q] : -1;
         st[q] = ok[q] ? atomicExch(d.stamp + i[q], d.batch_id) : 0;
-        cap0[q] = ok[q] ? ldv(d.cap + i[q]) : 0;
-        ri[q] = ok[q] ? d.rev[i[q]] : 0;
+        cap0[q] = ok[q] ? atomicExch(d.cap + i[q], c[q]) : 0;   // (entries naming one slot chain: their deltas add up)
       }
 #pragma unroll
       for (int q = 0; q < EU; q++) {
         if (!ok[q]) continue;
         const int64_t j = j0 + (int64_t)q * nt;
         const int32_t delta = c[q] - cap0[q];
-        atomicAdd(d.cap + i[q], delta);
         int32_t r = atomicAdd(d.res + i[q], delta) + delta;
         atomicAdd(d.rres + ri[q], delta);
         int32_t dd = 0, sat = 0;
