@@ -1,8 +1,15 @@
-// reach.cuh -- the S_min query (dmf_min_cut_source_side, reading R19):
-// S_min is the set of vertices reachable from {s} u {v != t : e(v) > 0} in the residual
-// graph of the converged state (c_f(u,v) = res[slot (u,v)] > 0).  It is the
-// intersection of all minimum cuts' source sides, unique, and it does not depend on
-// which maximum (pre)flow the engine holds.
+// reach.cuh -- k_reach, the two pure-BFS jobs of the engine:
+//  * k_reach<false>: the S_min query (dmf_min_cut_source_side, reading
+//    R19): S_min is the set of vertices reachable from {s} u {v != t : e(v) > 0} in the
+//    residual graph of the converged state (c_f(u,v) = res[slot (u,v)] > 0).  It
+//    is the intersection of all minimum cuts' source sides, unique, and it does not
+//    depend on which maximum (pre)flow the engine holds.
+//  * k_reach<true>: the universal certificate of a DYN_PP warm start (reading R9, H8):
+//    a fresh backward BFS from {t} u {v != s : e(v) < 0} on h+ must label no excess
+//    vertex, and s must reach no labelled vertex; then the state is converged, the
+//    partition is the labelled set (T', R15) and the epilogue writes it, F (R8) and the
+//    label histogram of the next warm start.  Otherwise it writes nothing and the
+//    MODE_PP_CONT launch of k_solve that follows runs the full Alg.8 stage 1.
 //
 // A lean level-synchronous, direction-optimising BFS in its OWN persistent cooperative
 // kernel: 256 threads and <= 40 registers per thread, i.e. 48 resident warps per SM --
