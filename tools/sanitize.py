@@ -49,4 +49,23 @@ for sched in ("async", "rounds", "topology"):
         b = W.rmat_batch(g, st, 0.02, 50 + j); st.apply(b)
         f.apply_batch(b.u, b.v, b.new_cap, algo="pp"); check(f, st.graph(), f"{sched} rmat10 b{j}")
     f.close()
+# warm DYN_PP chains (F and S_min only: an S_max query would end the warm start), so the
+# k_reach certificate, its failure path (MODE_PP_CONT), the back-off and the S_min query
+# kernel all run under the tool
+for knobs in (dict(), dict(schedule="async", budget_mul=-1000000, tail_items=1)):
+    g = W.rmat(10, 8, 1, 7)
+    f = P.DynMaxFlow.from_graph(g, **knobs)
+    f.static_solve()
+    st = W.CapState(g)
+    seen = set()
+    for j in range(8):
+        b = W.rmat_batch(g, st, 0.01 if j % 2 else 0.002, 80 + j); st.apply(b)
+        f.apply_batch(b.u, b.v, b.new_cap, algo="pp")
+        seen.add(f.stats()["certified"])
+        r = O.maxflow(st.graph(), "dinic")
+        if not (f.flow_value() == r["F"] and np.array_equal(f.min_cut_source_side(), r["smin"])):
+            fails += 1
+            print("MISMATCH warm", knobs, j, flush=True)
+    print("warm chain", knobs, "certificate outcomes", sorted(seen), flush=True)
+    f.close()
 print("sanitize workload done, mismatches:", fails)
