@@ -373,7 +373,7 @@ def run_reference(args):
     wall = time.time() - t0
     value = k * len(res) / wall if res else None
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": len(res), "warmup": 0, "ms_per_step": 1e3 * wall / max(1, len(res)),
+            "steps": len(res), "warmup": args.warmup, "ms_per_step": 1e3 * wall / max(1, len(res)),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
             "data": "synthetic", "config": config_dict(g.n, g.m, args, k),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": Pw, "kind": "oracle",
